@@ -1,0 +1,177 @@
+/*
+ * heom_b200.h -- C ABI of the B200-native HEOM propagator (libheomb200.so).
+ *
+ * Plain pointers and sizes only; complex arrays are interleaved (re, im) float64
+ * in C order, i.e. exactly numpy complex128.  Host buffers are owned by the
+ * caller; device buffers, the CUDA stream and the CUDA graph are owned by the
+ * handle.  Distinct handles may be driven from different threads concurrently
+ * (ctypes releases the GIL); one handle must not be used by two threads at once.
+ *
+ * Every entry point cites the reference interface it replaces
+ * (/root/reference/pkg/src/excitonflow/...).
+ *
+ * Return codes: HB_OK, or one of the HB_ERR_* / HB_DIVERGED / HB_HARDCAP codes;
+ * the message of the last failure on the calling thread is hb_last_error().
+ */
+#ifndef HEOM_B200_H
+#define HEOM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_OK 0
+#define HB_ERR_ARG 1      /* bad argument -> ValueError            */
+#define HB_ERR_CUDA 2     /* CUDA failure / no device             */
+#define HB_DIVERGED 3     /* heom.py:386-389 PropagationDiverged  */
+#define HB_HARDCAP 4      /* heom.py:366-368 ConvergenceFailure   */
+#define HB_ERR_RANGE 5    /* hierarchy.py:66-69 index range       */
+
+/* stop reasons (Trajectory.stop_reason, observables.py:33) */
+#define HB_STOP_NONE 0
+#define HB_STOP_T_END 1
+#define HB_STOP_RESIDUAL 2
+
+/* state layouts on the device */
+#define HB_LAYOUT_AUTO 0       /* Hermitian-packed if rho0 is exactly Hermitian */
+#define HB_LAYOUT_HERMITIAN 1  /* d*d real planes per ADO (upper triangle)     */
+#define HB_LAYOUT_GENERAL 2    /* 2*d*d real planes per ADO                     */
+
+/* ADO orderings on the device (the tables exported are always reference order) */
+#define HB_ORDER_LEX 0         /* pure lexicographic over all tiers (locality)  */
+#define HB_ORDER_REFERENCE 1   /* tier-major lexicographic (hierarchy.py:71-78) */
+
+#define HB_MAX_D 8
+#define HB_MAX_KP1 8
+#define HB_MAX_SINKS 4
+#define HB_MAX_SINK_TERMS 32
+
+/* Operands + stop policy of one propagation (heom.py:57-94 PropagationConfig,
+ * heom.py:235-275 _BlockPropagator.__init__, heom.py:121-134 loss channels). */
+typedef struct {
+    int d;                    /* block dimension (non-sink levels), 1..HB_MAX_D   */
+    int n_sites;              /* site slots (len(system.site_indices))            */
+    int kp1;                  /* modes per site = n_matsubara + 1                 */
+    int n_max;                /* truncation tier                                  */
+    const double* h;          /* d*d, rad/fs, mean-diagonal shifted (heom.py:251-255) */
+    const int32_t* site_of;   /* d: block position -> site slot or -1             */
+    const double* decay;      /* d: summed loss rate out of each position         */
+    const double* nu;         /* kp1: damping rate of Matsubara index k (fs^-1)   */
+    const double* a;          /* kp1: commutator weight of theta_k (fs^-2)        */
+    const double* b;          /* kp1: anticommutator weight of theta_k (fs^-2)    */
+    int n_sinks;              /* sinks integrated alongside (heom.py:282-283)     */
+    const int32_t* sink_nterms;   /* n_sinks                                      */
+    const double* sink_rate;      /* concatenated (rate, pos) terms, channel order */
+    const int32_t* sink_pos;
+    int n_site_pos;           /* residual sum positions (heom.py:352-353)         */
+    const int32_t* site_pos;
+    int d_full;               /* full basis dimension for records                 */
+    const int32_t* block_full;    /* d: full index of each block position          */
+    const int32_t* sink_full;     /* n_sinks: full index of each sink              */
+    double dt;
+    int has_t_end;
+    double t_end;
+    int has_residual;
+    double residual;
+    double hard_cap;
+    int64_t record_stride;
+    int record_matrices;
+    double blowup_norm;
+    int device;               /* CUDA device ordinal                              */
+    int layout;               /* HB_LAYOUT_*                                      */
+    int ordering;             /* HB_ORDER_*                                       */
+    int chunk_steps;          /* RK4 steps per CUDA-graph launch (0 = default)    */
+} hb_params;
+
+typedef struct {
+    int stop_reason;          /* HB_STOP_*                                        */
+    int layout;               /* layout actually used                             */
+    int64_t steps;            /* RK4 steps taken                                  */
+    int64_t n_records;        /* records available via hb_get_records             */
+    int64_t n_tot;            /* hierarchy size                                   */
+} hb_result;
+
+typedef struct hb_handle hb_handle;
+
+/* Last error message of the calling thread ("" if none). */
+const char* hb_last_error(void);
+
+/* Number of visible CUDA devices (0 when none / no driver). */
+int hb_device_count(void);
+
+/* hierarchy.py:27-29 hierarchy_size; -1 if the count overflows int64. */
+int64_t hb_hierarchy_size(int modes, int n_max);
+
+/* hierarchy.py:59-105 enumerate_hierarchy, built on the device.  All outputs in
+ * the reference order (tier-major lexicographic), int32, caller-allocated:
+ * indices/plus/minus (n_tot, modes), tiers (n_tot).  perm_or_null (n_tot)
+ * receives the device (HB_ORDER_LEX) position of every reference position.
+ * Errors: HB_ERR_ARG (modes < 1 or n_max < 0), HB_ERR_RANGE (n_tot > INT32_MAX). */
+int hb_graph_build(int modes, int n_max, int device, int32_t* indices, int32_t* tiers,
+                   int32_t* plus, int32_t* minus, int32_t* perm_or_null);
+
+/* ---- Level-2 kernel ABI (_kernels.py), host buffers, copies inside ---- */
+
+/* _kernels.py:23-58 hierarchy_rhs_kernel(out, sig, h, site_of, plus, minus, nvec,
+ * tier_damp, a_comm, b_anti, decay): sig/out (n_tot,d,d) complex128, plus/minus/
+ * nvec (n_tot,modes) with modes = number of site slots (one mode per site),
+ * nvec holding integers 0..255 (as float64, like the reference). */
+int hb_rhs(double* out, const double* sig, int64_t n_tot, int d, const double* h,
+           const int32_t* site_of, const int32_t* plus, const int32_t* minus, int modes,
+           const double* nvec, const double* tier_damp, double a_comm, double b_anti,
+           const double* decay, int device);
+
+/* _kernels.py:61-65 add_scaled: out = x + c*y over n complex elements. */
+int hb_add_scaled(double* out, const double* x, const double* y, double c, int64_t n,
+                  int device);
+/* _kernels.py:68-72 rk4_update: sig += w*(k1 + 2*(k2+k3) + k4). */
+int hb_rk4_update(double* sig, const double* k1, const double* k2, const double* k3,
+                  const double* k4, double w, int64_t n, int device);
+/* _kernels.py:75-84 max_abs2 -> *result. */
+int hb_max_abs2(const double* x, int64_t n, double* result, int device);
+
+/* ---- Level-1 propagator (heom.py:286-406 propagate_from) ---- */
+
+/* Allocate device state, build the hierarchy tables on the device. */
+int hb_create(const hb_params* params, hb_handle** out);
+void hb_destroy(hb_handle* h);
+
+/* rho0_block: d*d complex (block part of rho0), sink_pops: n_sinks.  Resets the
+ * run (step 0, auxiliaries 0), records the t=0 sample and evaluates the stop
+ * policy for step 0.  layout AUTO picks HERMITIAN when rho0_block is exactly
+ * Hermitian (diagonal imaginary parts zero), else GENERAL. */
+int hb_set_rho0(hb_handle* h, const double* rho0_block, const double* sink_pops);
+
+/* Run until a stop policy fires (heom.py:358-391).  Returns HB_OK with
+ * res->stop_reason set, HB_DIVERGED (res->steps = step whose guard fired) or
+ * HB_HARDCAP. */
+int hb_run(hb_handle* h, hb_result* res);
+
+/* Records collected by hb_set_rho0 + hb_run: steps (n), pops (n*d_full),
+ * mats_or_null (n*d_full*d_full complex; requires record_matrices).  cap = room. */
+int hb_get_records(hb_handle* h, int64_t* steps, double* pops, double* mats_or_null,
+                   int64_t cap);
+
+/* Current state in the reference order and layout: sig (n_tot,d,d) complex,
+ * sink_pops (n_sinks). */
+int hb_get_state(hb_handle* h, double* sig, double* sink_pops);
+
+/* sigma^0 only (the reduced density matrix block, d*d complex) and the sinks:
+ * what Trajectory.final_rho needs (heom.py:343-350) without copying the state. */
+int hb_get_sigma0(hb_handle* h, double* sig0, double* sink_pops);
+
+/* Benchmark / profiling helpers (bench.py).  Run exactly n_steps RK4 steps on
+ * the resident state ignoring the stop policy; *ms = CUDA-event time on the
+ * handle's stream.  stage_ms_or_null[4] (optional) receives the average time of
+ * each stage kernel, measured with events around individual launches. */
+int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms_or_null);
+
+/* Device-side launch count of product kernels since hb_create. */
+int64_t hb_launch_count(hb_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEOM_B200_H */

@@ -1,0 +1,688 @@
+// C ABI of libheomb200.so (see include/heom_b200.h).
+//
+// The handle owns the device state of one propagation: the hierarchy tables
+// (built on the device, hb_graph.cu), four AoSoA state buffers (sigma, Y2, Y3,
+// Y4), the control block, the record buffer, a private CUDA stream and a CUDA
+// graph of `chunk_steps` RK4 steps (4 stage kernels each).  hb_run replays the
+// graph and synchronises once per chunk to drain records and read the status
+// written by the last CTA of each stage-4 kernel (hb_stage.cu).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include "hb_internal.h"
+
+using namespace hb;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static int cuda_fail(cudaError_t e, const char* where) {
+  cudaGetLastError();  // clear sticky-free errors
+  return fail(HB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CK(x)                                   \
+  do {                                          \
+    cudaError_t e_ = (x);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
+  } while (0)
+
+struct hb_handle {
+  hb_params prm{};
+  std::vector<double> h, decay, nu, a, b, sink_rate;
+  std::vector<int32_t> site_of, sink_nterms, sink_pos, site_pos, block_full, sink_full;
+  int device = 0;
+  int modes = 0, n_tot = 0, n_tiles = 0;
+  int chunk = 64;
+  cudaStream_t stream = nullptr;
+  GraphTables gt;
+  int layout = 0;  // HB_LAYOUT_HERMITIAN / GENERAL once allocated
+  int n_planes = 0;
+  double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // sigma, Y2, Y3, Y4
+  Ctl* ctl = nullptr;
+  Ctl* ctl_host = nullptr;  // pinned
+  long long* rec_step = nullptr;
+  double* rec_pops = nullptr;
+  double* rec_mats = nullptr;
+  long long rec_cap = 0;
+  KParams base{};
+  cudaGraphExec_t graph = nullptr;
+  int graph_layout = -1;
+  std::vector<int64_t> steps;
+  std::vector<double> pops, mats;
+  int64_t launches = 0;
+  bool ready = false;  // rho0 set
+};
+
+// definitions take C linkage from the extern "C" declarations in heom_b200.h
+
+const char* hb_last_error(void) { return g_err.c_str(); }
+
+int hb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int64_t hb_hierarchy_size(int modes, int n_max) { return hierarchy_size(modes, n_max); }
+
+static int check_graph_args(int modes, int n_max, int64_t* n_tot) {
+  if (modes < 1) return fail(HB_ERR_ARG, "need at least one site");
+  if (n_max < 0) return fail(HB_ERR_ARG, "truncation tier must be >= 0");
+  if (modes > MAX_MODES) return fail(HB_ERR_ARG, "more than 64 modes is not supported");
+  const int64_t n = hierarchy_size(modes, n_max);
+  if (n < 0 || n > INT32_MAX) {
+    char buf[160];
+    if (n < 0)
+      snprintf(buf, sizeof buf, "hierarchy with more than 2^63 indices exceeds the supported index range");
+    else
+      snprintf(buf, sizeof buf, "hierarchy with %lld indices exceeds the supported index range",
+               (long long)n);
+    return fail(HB_ERR_RANGE, buf);
+  }
+  *n_tot = n;
+  return HB_OK;
+}
+
+int hb_graph_build(int modes, int n_max, int device, int32_t* indices, int32_t* tiers,
+                   int32_t* plus, int32_t* minus, int32_t* perm_or_null) {
+  int64_t n_tot = 0;
+  int rc = check_graph_args(modes, n_max, &n_tot);
+  if (rc) return rc;
+  CK(cudaSetDevice(device));
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = build_graph(modes, n_max, HB_ORDER_LEX, s, indices, tiers, plus, minus,
+                              perm_or_null, nullptr);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess) return cuda_fail(e, "build_graph");
+  return HB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Level-2 kernel ABI shims
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n ? n : 8); }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+int hb_rhs(double* out, const double* sig, int64_t n_tot, int d, const double* h,
+           const int32_t* site_of, const int32_t* plus, const int32_t* minus, int modes,
+           const double* nvec, const double* tier_damp, double a_comm, double b_anti,
+           const double* decay, int device) {
+  if (d < 1 || d > MAXD) return fail(HB_ERR_ARG, "block dimension must be 1..8");
+  if (n_tot < 1 || n_tot > INT32_MAX) return fail(HB_ERR_ARG, "bad n_tot");
+  if (modes < 1 || modes > MAX_MODES) return fail(HB_ERR_ARG, "bad mode count");
+  std::vector<uint8_t> nv((size_t)n_tot * modes);
+  for (size_t i = 0; i < nv.size(); ++i) {
+    const double v = nvec[i];
+    if (!(v >= 0.0 && v <= 255.0 && v == std::floor(v)))
+      return fail(HB_ERR_ARG, "nvec must hold integers 0..255");
+    nv[i] = (uint8_t)v;
+  }
+  CK(cudaSetDevice(device));
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
+  GraphTables gt;
+  struct GG { GraphTables* g; ~GG() { free_graph(g); } } gg{&gt};
+  CK(upload_tables(modes, (int)n_tot, plus, minus, nv.data(), s, &gt));
+  KParams p{};
+  p.d = d;
+  p.n_sites = modes;
+  p.kp1 = 1;
+  p.modes = modes;
+  p.n_tot = (int)n_tot;
+  p.n_tiles = gt.n_tiles;
+  p.hermitian = 0;
+  p.n_planes = 2 * d * d;
+  for (int i = 0; i < d; ++i) {
+    for (int j = 0; j < d; ++j) p.h[i * MAXD + j] = h[i * d + j];
+    p.site_of[i] = site_of[i];
+    p.decay[i] = decay[i];
+  }
+  p.a[0] = a_comm;
+  p.b[0] = b_anti;
+  const size_t n_pad = (size_t)gt.n_tiles * TILE;
+  const size_t ref_bytes = (size_t)n_tot * d * d * 2 * sizeof(double);
+  const size_t dev_bytes = n_pad * p.n_planes * sizeof(double);
+  DevBuf dref, din, dout, ddamp;
+  CK(dref.alloc(ref_bytes));
+  CK(din.alloc(dev_bytes));
+  CK(dout.alloc(dev_bytes));
+  CK(ddamp.alloc(n_pad * sizeof(double)));
+  CK(cudaMemsetAsync(ddamp.p, 0, n_pad * sizeof(double), s));
+  CK(cudaMemcpyAsync(ddamp.p, tier_damp, (size_t)n_tot * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dref.p, sig, ref_bytes, cudaMemcpyHostToDevice, s));
+  CK(launch_pack(p, dref.as<double>(), gt.dev2ref, din.as<double>(), s));
+  p.Yin = din.as<double>();
+  p.Yout = dout.as<double>();
+  p.plus = gt.plus_t;
+  p.minus = gt.minus_t;
+  p.nvec = gt.nvec_t;
+  p.damp_plane = ddamp.as<double>();
+  CK(configure_stages(p));
+  CK(launch_rhs_only(p, s));
+  CK(launch_unpack(p, dout.as<double>(), gt.dev2ref, dref.as<double>(), s));
+  CK(cudaMemcpyAsync(out, dref.p, ref_bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return HB_OK;
+}
+
+static int elementwise(int op, double* out, const double* x, const double* y, const double* z,
+                       const double* w, double c, int64_t n, int device) {
+  if (n < 0) return fail(HB_ERR_ARG, "negative size");
+  if (n == 0) return HB_OK;
+  CK(cudaSetDevice(device));
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
+  const size_t bytes = (size_t)n * 2 * sizeof(double);
+  DevBuf o, a, b, cc, dd;
+  CK(o.alloc(bytes));
+  CK(a.alloc(bytes));
+  CK(b.alloc(bytes));
+  CK(cudaMemcpyAsync(a.p, x, bytes, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(b.p, y, bytes, cudaMemcpyHostToDevice, s));
+  if (op == 1) {
+    CK(cc.alloc(bytes));
+    CK(dd.alloc(bytes));
+    CK(cudaMemcpyAsync(o.p, out, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(cc.p, z, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dd.p, w, bytes, cudaMemcpyHostToDevice, s));
+  }
+  CK(launch_elementwise(op, n, o.as<double>(), a.as<double>(), b.as<double>(), cc.as<double>(),
+                        dd.as<double>(), c, s));
+  CK(cudaMemcpyAsync(out, o.p, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return HB_OK;
+}
+
+int hb_add_scaled(double* out, const double* x, const double* y, double c, int64_t n, int device) {
+  return elementwise(0, out, x, y, nullptr, nullptr, c, n, device);
+}
+
+int hb_rk4_update(double* sig, const double* k1, const double* k2, const double* k3,
+                  const double* k4, double w, int64_t n, int device) {
+  return elementwise(1, sig, k1, k2, k3, k4, w, n, device);
+}
+
+int hb_max_abs2(const double* x, int64_t n, double* result, int device) {
+  if (n < 0) return fail(HB_ERR_ARG, "negative size");
+  *result = 0.0;
+  if (n == 0) return HB_OK;
+  CK(cudaSetDevice(device));
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
+  const size_t bytes = (size_t)n * 2 * sizeof(double);
+  DevBuf a, r;
+  CK(a.alloc(bytes));
+  CK(r.alloc(sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(r.p, 0, sizeof(unsigned long long), s));
+  CK(cudaMemcpyAsync(a.p, x, bytes, cudaMemcpyHostToDevice, s));
+  CK(launch_max_abs2(n, a.as<double>(), r.as<unsigned long long>(), s));
+  unsigned long long bits = 0;
+  CK(cudaMemcpyAsync(&bits, r.p, sizeof bits, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::memcpy(result, &bits, sizeof(double));
+  return HB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Level-1 propagator
+
+static void free_state(hb_handle* h) {
+  for (auto& b : h->buf) {
+    if (b) cudaFree(b);
+    b = nullptr;
+  }
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  h->graph = nullptr;
+  h->graph_layout = -1;
+}
+
+void hb_destroy(hb_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  free_state(h);
+  free_graph(&h->gt);
+  cudaFree(h->ctl);
+  cudaFreeHost(h->ctl_host);
+  cudaFree(h->rec_step);
+  cudaFree(h->rec_pops);
+  cudaFree(h->rec_mats);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int hb_create(const hb_params* P, hb_handle** out) {
+  *out = nullptr;
+  if (!P) return fail(HB_ERR_ARG, "null params");
+  const hb_params& q = *P;
+  if (q.d < 1 || q.d > MAXD) return fail(HB_ERR_ARG, "block dimension must be 1..8");
+  if (q.kp1 < 1 || q.kp1 > MAXKP1) return fail(HB_ERR_ARG, "n_matsubara must be 0..7");
+  if (q.n_max > 255) return fail(HB_ERR_ARG, "n_max > 255 is not supported");
+  if (q.n_sinks < 0 || q.n_sinks > MAXS) return fail(HB_ERR_ARG, "too many sinks");
+  if (q.n_site_pos < 0 || q.n_site_pos > MAXD) return fail(HB_ERR_ARG, "bad site positions");
+  if (q.d_full < q.d) return fail(HB_ERR_ARG, "d_full < d");
+  if (!(q.dt > 0)) return fail(HB_ERR_ARG, "dt must be > 0");
+  if (q.record_stride < 1) return fail(HB_ERR_ARG, "record stride must be >= 1");
+  int nterms = 0;
+  for (int s = 0; s < q.n_sinks; ++s) nterms += q.sink_nterms[s];
+  if (nterms > MAXT) return fail(HB_ERR_ARG, "too many sink terms");
+  const int modes = q.n_sites * q.kp1;
+  int64_t n_tot = 0;
+  int rc = check_graph_args(modes, q.n_max, &n_tot);
+  if (rc) return rc;
+
+  hb_handle* h = new hb_handle();
+  h->prm = q;
+  h->device = q.device;
+  h->modes = modes;
+  h->n_tot = (int)n_tot;
+  h->chunk = q.chunk_steps > 0 ? q.chunk_steps : 64;
+  const int d = q.d;
+  h->h.assign(q.h, q.h + d * d);
+  h->decay.assign(q.decay, q.decay + d);
+  h->site_of.assign(q.site_of, q.site_of + d);
+  h->nu.assign(q.nu, q.nu + q.kp1);
+  h->a.assign(q.a, q.a + q.kp1);
+  h->b.assign(q.b, q.b + q.kp1);
+  h->sink_nterms.assign(q.sink_nterms, q.sink_nterms + q.n_sinks);
+  h->sink_rate.assign(q.sink_rate, q.sink_rate + nterms);
+  h->sink_pos.assign(q.sink_pos, q.sink_pos + nterms);
+  h->site_pos.assign(q.site_pos, q.site_pos + q.n_site_pos);
+  h->block_full.assign(q.block_full, q.block_full + d);
+  h->sink_full.assign(q.sink_full, q.sink_full + q.n_sinks);
+  for (int i = 0; i < d; ++i)
+    if (h->site_of[i] >= q.n_sites) {
+      delete h;
+      return fail(HB_ERR_ARG, "site_of out of range");
+    }
+  auto bail = [&](cudaError_t e, const char* w) {
+    int r = cuda_fail(e, w);
+    hb_destroy(h);
+    return r;
+  };
+  cudaError_t e = cudaSetDevice(h->device);
+  if (e) return bail(e, "cudaSetDevice");
+  e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e) return bail(e, "cudaStreamCreate");
+  e = build_graph(modes, q.n_max, q.ordering, h->stream, nullptr, nullptr, nullptr, nullptr,
+                  nullptr, &h->gt);
+  if (e) return bail(e, "build_graph");
+  h->n_tiles = h->gt.n_tiles;
+  e = cudaMalloc(&h->ctl, sizeof(Ctl));
+  if (e) return bail(e, "cudaMalloc(ctl)");
+  e = cudaMallocHost(&h->ctl_host, sizeof(Ctl));
+  if (e) return bail(e, "cudaMallocHost(ctl)");
+  h->rec_cap = h->chunk + 4;
+  e = cudaMalloc(&h->rec_step, h->rec_cap * sizeof(long long));
+  if (!e) e = cudaMalloc(&h->rec_pops, h->rec_cap * q.d_full * sizeof(double));
+  if (!e && q.record_matrices)
+    e = cudaMalloc(&h->rec_mats, h->rec_cap * q.d_full * q.d_full * 2 * sizeof(double));
+  if (e) return bail(e, "cudaMalloc(records)");
+
+  KParams& p = h->base;
+  p.d = d;
+  p.n_sites = q.n_sites;
+  p.kp1 = q.kp1;
+  p.modes = modes;
+  p.n_tot = h->n_tot;
+  p.n_tiles = h->n_tiles;
+  p.tile_begin = 0;
+  for (int i = 0; i < d; ++i) {
+    for (int j = 0; j < d; ++j) p.h[i * MAXD + j] = h->h[i * d + j];
+    p.decay[i] = h->decay[i];
+    p.site_of[i] = h->site_of[i];
+    p.block_full[i] = h->block_full[i];
+  }
+  for (int k = 0; k < q.kp1; ++k) {
+    p.nu[k] = h->nu[k];
+    p.a[k] = h->a[k];
+    p.b[k] = h->b[k];
+  }
+  p.plus = h->gt.plus_t;
+  p.minus = h->gt.minus_t;
+  p.nvec = h->gt.nvec_t;
+  p.damp_plane = nullptr;
+  p.dt = q.dt;
+  p.ctl = h->ctl;
+  p.n_sinks = q.n_sinks;
+  for (int s = 0; s < q.n_sinks; ++s) {
+    p.sink_nterms[s] = h->sink_nterms[s];
+    p.sink_full[s] = h->sink_full[s];
+  }
+  for (int t = 0; t < nterms; ++t) {
+    p.sink_rate[t] = h->sink_rate[t];
+    p.sink_pos[t] = h->sink_pos[t];
+  }
+  p.n_site_pos = q.n_site_pos;
+  for (int k = 0; k < q.n_site_pos; ++k) p.site_pos[k] = h->site_pos[k];
+  p.d_full = q.d_full;
+  p.has_t_end = q.has_t_end;
+  p.has_residual = q.has_residual;
+  p.record_matrices = q.record_matrices;
+  p.t_end = q.t_end;
+  p.residual = q.residual;
+  p.hard_cap = q.hard_cap;
+  p.blow2 = q.blowup_norm * q.blowup_norm;
+  p.stride = q.record_stride;
+  p.rec_cap = h->rec_cap;
+  p.rec_step = h->rec_step;
+  p.rec_pops = h->rec_pops;
+  p.rec_mats = h->rec_mats;
+  *out = h;
+  return HB_OK;
+}
+
+static KParams stage_params(hb_handle* h, int stage) {
+  KParams p = h->base;
+  double* S = h->buf[0];
+  double* Y2 = h->buf[1];
+  double* Y3 = h->buf[2];
+  double* Y4 = h->buf[3];
+  p.sig = S;
+  p.Y2 = Y2;
+  p.Y3 = Y3;
+  const double dt = h->prm.dt;
+  switch (stage) {
+    case 1: p.Yin = S;  p.Yout = Y2; p.coef = 0.5 * dt; break;
+    case 2: p.Yin = Y2; p.Yout = Y3; p.coef = 0.5 * dt; break;
+    case 3: p.Yin = Y3; p.Yout = Y4; p.coef = dt; break;
+    default: p.Yin = Y4; p.Yout = S; p.coef = dt; break;
+  }
+  return p;
+}
+
+static int alloc_state(hb_handle* h, int layout) {
+  if (h->layout == layout && h->buf[0]) return HB_OK;
+  free_state(h);
+  h->layout = layout;
+  const int d = h->prm.d;
+  h->n_planes = layout == HB_LAYOUT_HERMITIAN ? d * d : 2 * d * d;
+  const size_t bytes = (size_t)h->n_tiles * TILE * h->n_planes * sizeof(double);
+  for (auto& b : h->buf) {
+    CK(cudaMalloc(&b, bytes));
+    CK(cudaMemsetAsync(b, 0, bytes, h->stream));
+  }
+  h->base.hermitian = layout == HB_LAYOUT_HERMITIAN;
+  h->base.n_planes = h->n_planes;
+  CK(configure_stages(h->base));
+  return HB_OK;
+}
+
+static int drain(hb_handle* h) {
+  // ctl_host is current (caller synchronised)
+  const long long n = h->ctl_host->n_rec;
+  if (n <= 0) return HB_OK;
+  const int df = h->prm.d_full;
+  const size_t s0 = h->steps.size();
+  h->steps.resize(s0 + n);
+  h->pops.resize((s0 + n) * df);
+  std::vector<long long> st(n);
+  CK(cudaMemcpyAsync(st.data(), h->rec_step, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(h->pops.data() + s0 * df, h->rec_pops, n * df * sizeof(double),
+                     cudaMemcpyDeviceToHost, h->stream));
+  if (h->prm.record_matrices) {
+    h->mats.resize((s0 + n) * df * df * 2);
+    CK(cudaMemcpyAsync(h->mats.data() + s0 * df * df * 2, h->rec_mats,
+                       n * df * df * 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  }
+  const long long zero = 0;
+  CK(cudaMemcpyAsync(&h->ctl->n_rec, &zero, sizeof zero, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  for (long long i = 0; i < n; ++i) h->steps[s0 + i] = st[i];
+  h->ctl_host->n_rec = 0;
+  return HB_OK;
+}
+
+static int sync_ctl(hb_handle* h) {
+  CK(cudaMemcpyAsync(h->ctl_host, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return HB_OK;
+}
+
+int hb_set_rho0(hb_handle* h, const double* rho0, const double* sink_pops) {
+  if (!h) return fail(HB_ERR_ARG, "null handle");
+  CK(cudaSetDevice(h->device));
+  const int d = h->prm.d;
+  int layout = h->prm.layout;
+  if (layout == HB_LAYOUT_AUTO) {
+    bool herm = true;
+    for (int i = 0; i < d && herm; ++i)
+      for (int j = 0; j < d; ++j) {
+        const double re = rho0[2 * (i * d + j)], im = rho0[2 * (i * d + j) + 1];
+        const double rt = rho0[2 * (j * d + i)], it = rho0[2 * (j * d + i) + 1];
+        if (re != rt || im != -it) {
+          herm = false;
+          break;
+        }
+      }
+    layout = herm ? HB_LAYOUT_HERMITIAN : HB_LAYOUT_GENERAL;
+  }
+  int rc = alloc_state(h, layout);
+  if (rc) return rc;
+  // sigma: auxiliaries zero, sigma^0 = rho0 block in tile 0, lane 0
+  const size_t bytes = (size_t)h->n_tiles * TILE * h->n_planes * sizeof(double);
+  CK(cudaMemsetAsync(h->buf[0], 0, bytes, h->stream));
+  std::vector<double> tile0((size_t)h->n_planes * TILE, 0.0);
+  if (layout == HB_LAYOUT_HERMITIAN) {
+    int e = d;
+    for (int i = 0; i < d; ++i) tile0[(size_t)i * TILE] = rho0[2 * (i * d + i)];
+    for (int i = 0; i < d; ++i)
+      for (int j = i + 1; j < d; ++j, ++e) {
+        const int pr = d + 2 * (e - d);
+        tile0[(size_t)pr * TILE] = rho0[2 * (i * d + j)];
+        tile0[(size_t)(pr + 1) * TILE] = rho0[2 * (i * d + j) + 1];
+      }
+  } else {
+    for (int k = 0; k < d * d; ++k) {
+      tile0[(size_t)(2 * k) * TILE] = rho0[2 * k];
+      tile0[(size_t)(2 * k + 1) * TILE] = rho0[2 * k + 1];
+    }
+  }
+  CK(cudaMemcpyAsync(h->buf[0], tile0.data(), tile0.size() * sizeof(double),
+                     cudaMemcpyHostToDevice, h->stream));
+  Ctl c{};
+  c.status = ST_RUNNING;
+  for (int s = 0; s < h->prm.n_sinks; ++s) c.sink_pops[s] = sink_pops[s];
+  std::memcpy(h->ctl_host, &c, sizeof c);
+  CK(cudaMemcpyAsync(h->ctl, h->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
+  h->steps.clear();
+  h->pops.clear();
+  h->mats.clear();
+  KParams p = stage_params(h, 4);
+  CK(launch_init(p, h->stream));
+  h->launches += 1;
+  rc = sync_ctl(h);
+  if (rc) return rc;
+  rc = drain(h);
+  if (rc) return rc;
+  h->ready = true;
+  return HB_OK;
+}
+
+static int ensure_graph(hb_handle* h) {
+  if (h->graph && h->graph_layout == h->layout) return HB_OK;
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  h->graph = nullptr;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t err = cudaSuccess;
+  for (int c = 0; c < h->chunk && !err; ++c)
+    for (int s = 1; s <= 4 && !err; ++s) err = launch_stage(s, stage_params(h, s), h->stream);
+  cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
+  if (err) return cuda_fail(err, "capture stage kernels");
+  if (e2) return cuda_fail(e2, "cudaStreamEndCapture");
+  err = cudaGraphInstantiate(&h->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (err) return cuda_fail(err, "cudaGraphInstantiate");
+  h->graph_layout = h->layout;
+  return HB_OK;
+}
+
+int hb_run(hb_handle* h, hb_result* res) {
+  if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
+  CK(cudaSetDevice(h->device));
+  int rc = ensure_graph(h);
+  if (rc) return rc;
+  while (h->ctl_host->status == ST_RUNNING) {
+    CK(cudaGraphLaunch(h->graph, h->stream));
+    h->launches += 4LL * h->chunk;
+    rc = sync_ctl(h);
+    if (rc) return rc;
+    rc = drain(h);
+    if (rc) return rc;
+  }
+  const Ctl& c = *h->ctl_host;
+  if (res) {
+    res->stop_reason = c.status == ST_T_END ? HB_STOP_T_END
+                       : c.status == ST_RESIDUAL ? HB_STOP_RESIDUAL : HB_STOP_NONE;
+    res->layout = h->layout;
+    res->steps = c.step;
+    res->n_records = (int64_t)h->steps.size();
+    res->n_tot = h->n_tot;
+  }
+  if (c.status == ST_DIVERGED) return fail(HB_DIVERGED, "matrix norm exceeded the blow-up bound");
+  if (c.status == ST_HARDCAP) return fail(HB_HARDCAP, "residual policy not reached within the cap");
+  return HB_OK;
+}
+
+int hb_get_records(hb_handle* h, int64_t* steps, double* pops, double* mats_or_null, int64_t cap) {
+  if (!h) return fail(HB_ERR_ARG, "null handle");
+  const int64_t n = (int64_t)h->steps.size();
+  if (cap < n) return fail(HB_ERR_ARG, "record buffer too small");
+  const int df = h->prm.d_full;
+  if (steps) std::memcpy(steps, h->steps.data(), n * sizeof(int64_t));
+  if (pops) std::memcpy(pops, h->pops.data(), n * df * sizeof(double));
+  if (mats_or_null) {
+    if (!h->prm.record_matrices) return fail(HB_ERR_ARG, "matrices were not recorded");
+    std::memcpy(mats_or_null, h->mats.data(), n * df * df * 2 * sizeof(double));
+  }
+  return HB_OK;
+}
+
+int hb_get_state(hb_handle* h, double* sig, double* sink_pops) {
+  if (!h || !h->ready) return fail(HB_ERR_ARG, "no state");
+  CK(cudaSetDevice(h->device));
+  const int d = h->prm.d;
+  const size_t ref_bytes = (size_t)h->n_tot * d * d * 2 * sizeof(double);
+  if (sig) {
+    DevBuf tmp;
+    CK(tmp.alloc(ref_bytes));
+    KParams p = h->base;
+    CK(launch_unpack(p, h->buf[0], h->gt.dev2ref, tmp.as<double>(), h->stream));
+    CK(cudaMemcpyAsync(sig, tmp.p, ref_bytes, cudaMemcpyDeviceToHost, h->stream));
+  }
+  int rc = sync_ctl(h);
+  if (rc) return rc;
+  if (sink_pops)
+    for (int s = 0; s < h->prm.n_sinks; ++s) sink_pops[s] = h->ctl_host->sink_pops[s];
+  return HB_OK;
+}
+
+int hb_get_sigma0(hb_handle* h, double* sig0, double* sink_pops) {
+  if (!h || !h->ready) return fail(HB_ERR_ARG, "no state");
+  CK(cudaSetDevice(h->device));
+  const int d = h->prm.d;
+  std::vector<double> tile0((size_t)h->n_planes * TILE);
+  CK(cudaMemcpyAsync(tile0.data(), h->buf[0], tile0.size() * sizeof(double),
+                     cudaMemcpyDeviceToHost, h->stream));
+  int rc = sync_ctl(h);
+  if (rc) return rc;
+  auto at = [&](int plane) { return tile0[(size_t)plane * TILE]; };  // lane 0 = ADO 0
+  if (h->layout == HB_LAYOUT_HERMITIAN) {
+    for (int i = 0; i < d; ++i) {
+      sig0[2 * (i * d + i)] = at(i);
+      sig0[2 * (i * d + i) + 1] = 0.0;
+    }
+    int e = d;
+    for (int i = 0; i < d; ++i)
+      for (int j = i + 1; j < d; ++j, ++e) {
+        const int pr = d + 2 * (e - d);
+        sig0[2 * (i * d + j)] = at(pr);
+        sig0[2 * (i * d + j) + 1] = at(pr + 1);
+        sig0[2 * (j * d + i)] = at(pr);
+        sig0[2 * (j * d + i) + 1] = -at(pr + 1);
+      }
+  } else {
+    for (int k = 0; k < 2 * d * d; ++k) sig0[k] = at(k);
+  }
+  if (sink_pops)
+    for (int s = 0; s < h->prm.n_sinks; ++s) sink_pops[s] = h->ctl_host->sink_pops[s];
+  return HB_OK;
+}
+
+int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
+  if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
+  if (h->ctl_host->status != ST_RUNNING) return fail(HB_ERR_ARG, "run already stopped");
+  CK(cudaSetDevice(h->device));
+  int rc = ensure_graph(h);
+  if (rc) return rc;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  struct EG { cudaEvent_t a, b; ~EG() { cudaEventDestroy(a); cudaEventDestroy(b); } } eg{e0, e1};
+  CK(cudaEventRecord(e0, h->stream));
+  int64_t left = n_steps;
+  while (left >= h->chunk) {
+    CK(cudaGraphLaunch(h->graph, h->stream));
+    h->launches += 4LL * h->chunk;
+    left -= h->chunk;
+  }
+  for (; left > 0; --left)
+    for (int s = 1; s <= 4; ++s) {
+      CK(launch_stage(s, stage_params(h, s), h->stream));
+      h->launches += 1;
+    }
+  CK(cudaEventRecord(e1, h->stream));
+  CK(cudaEventSynchronize(e1));
+  float f = 0.f;
+  CK(cudaEventElapsedTime(&f, e0, e1));
+  *ms = f;
+  if (stage_ms) {
+    // per-stage kernel durations: events around individual launches
+    const int reps = 8;
+    std::vector<cudaEvent_t> ev(reps * 5);
+    for (auto& x : ev) CK(cudaEventCreate(&x));
+    for (int r = 0; r < reps; ++r) {
+      CK(cudaEventRecord(ev[r * 5], h->stream));
+      for (int s = 1; s <= 4; ++s) {
+        CK(launch_stage(s, stage_params(h, s), h->stream));
+        h->launches += 1;
+        CK(cudaEventRecord(ev[r * 5 + s], h->stream));
+      }
+    }
+    CK(cudaEventSynchronize(ev.back()));
+    for (int s = 0; s < 4; ++s) stage_ms[s] = 0.0;
+    for (int r = 0; r < reps; ++r)
+      for (int s = 1; s <= 4; ++s) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, ev[r * 5 + s - 1], ev[r * 5 + s]));
+        stage_ms[s - 1] += t / reps;
+      }
+    for (auto& x : ev) cudaEventDestroy(x);
+  }
+  rc = sync_ctl(h);
+  if (rc) return rc;
+  rc = drain(h);
+  if (rc) return rc;
+  if (h->ctl_host->status != ST_RUNNING)
+    return fail(HB_ERR_ARG, "stop policy fired during timing; use a t_end beyond the timed steps");
+  return HB_OK;
+}
+
+int64_t hb_launch_count(hb_handle* h) { return h ? h->launches : 0; }

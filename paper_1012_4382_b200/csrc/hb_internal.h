@@ -1,0 +1,114 @@
+// Internal interfaces shared by the CUDA translation units of libheomb200.so.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "heom_b200.h"
+
+namespace hb {
+
+constexpr int TILE = 32;          // ADOs per tile (AoSoA inner extent = one warp)
+constexpr int MAXD = HB_MAX_D;
+constexpr int MAXKP1 = HB_MAX_KP1;
+constexpr int MAXS = HB_MAX_SINKS;
+constexpr int MAXT = HB_MAX_SINK_TERMS;
+constexpr int MAX_MODES = 64;
+
+enum Status : int {
+  ST_RUNNING = 0,
+  ST_T_END = 1,
+  ST_RESIDUAL = 2,
+  ST_DIVERGED = 3,
+  ST_HARDCAP = 4,
+};
+
+// Device-resident control block of one run (one per handle).
+struct Ctl {
+  int status;
+  int pad0;
+  long long step;
+  double sink_pops[MAXS];
+  double r[4][MAXS];                  // sink rates of the four stage inputs
+  unsigned long long maxabs2_bits;    // max |x|^2 over all ADOs (every 25 steps)
+  unsigned int blocks_done;           // last-block election counter
+  unsigned int pad1;
+  long long n_rec;                    // records in the device record buffer
+  long long launches;                 // product-kernel launches that did work
+};
+
+// Everything a stage kernel needs; passed by value (lives in the constant bank).
+struct KParams {
+  // operands
+  double h[MAXD * MAXD];
+  double decay[MAXD];
+  int site_of[MAXD];
+  double nu[MAXKP1], a[MAXKP1], b[MAXKP1];
+  int d, n_sites, kp1, modes;
+  int n_tot, n_tiles, tile_begin, n_planes;
+  // state (AoSoA: [tile][plane][32] doubles)
+  const double* Yin;     // stage input: own tile + gathers
+  const double* sig;     // sigma (stages 2-4)
+  const double* Y2;      // stage 4
+  const double* Y3;      // stage 4
+  double* Yout;          // Y_{s+1} (stages 1-3), sigma (stage 4), k (rhs-only)
+  // tables (AoSoA: [tile][mode][32])
+  const int32_t* plus;
+  const int32_t* minus;
+  const uint8_t* nvec;
+  const double* damp_plane;  // optional per-ADO damping (Level-2 shim), else null
+  double coef;               // dt/2, dt/2, dt for stages 1-3
+  double dt;
+  // bookkeeping
+  Ctl* ctl;
+  int n_sinks;
+  int sink_nterms[MAXS];
+  double sink_rate[MAXT];
+  int sink_pos[MAXT];
+  int n_site_pos;
+  int site_pos[MAXD];
+  int d_full;
+  int block_full[MAXD];
+  int sink_full[MAXS];
+  int has_t_end, has_residual, record_matrices, hermitian;
+  double t_end, residual, hard_cap, blow2;
+  long long stride;
+  long long rec_cap;
+  long long* rec_step;
+  double* rec_pops;
+  double* rec_mats;
+};
+
+// hb_stage.cu
+cudaError_t launch_stage(int stage, const KParams& p, cudaStream_t s);
+cudaError_t launch_rhs_only(const KParams& p, cudaStream_t s);
+cudaError_t configure_stages(const KParams& p);
+cudaError_t launch_init(const KParams& p, cudaStream_t s);
+cudaError_t launch_pack(const KParams& p, const double* ref_sig, const int32_t* dev2ref,
+                        double* dst, cudaStream_t s);
+cudaError_t launch_unpack(const KParams& p, const double* src, const int32_t* dev2ref,
+                          double* ref_sig, cudaStream_t s);
+cudaError_t launch_elementwise(int op, int64_t n, double* out, const double* x,
+                               const double* y, const double* z, const double* w, double c,
+                               cudaStream_t s);
+cudaError_t launch_max_abs2(int64_t n, const double* x, unsigned long long* bits,
+                            cudaStream_t s);
+
+// hb_graph.cu
+struct GraphTables {
+  int modes, n_max, n_tot, n_tiles;
+  int32_t* plus_t = nullptr;    // device, AoSoA [tile][mode][32], device ordering
+  int32_t* minus_t = nullptr;
+  uint8_t* nvec_t = nullptr;
+  int32_t* dev2ref = nullptr;   // device position -> reference position
+};
+int64_t hierarchy_size(int modes, int n_max);
+// builds the reference-order tables (host outputs may be null) and, if gt != null,
+// the device-order AoSoA tables.  ordering: HB_ORDER_*.
+cudaError_t build_graph(int modes, int n_max, int ordering, cudaStream_t s,
+                        int32_t* h_indices, int32_t* h_tiers, int32_t* h_plus, int32_t* h_minus,
+                        int32_t* h_perm, GraphTables* gt);
+void free_graph(GraphTables* gt);
+// converts caller tables in reference order (n_tot, modes) into AoSoA device tables
+cudaError_t upload_tables(int modes, int n_tot, const int32_t* plus, const int32_t* minus,
+                          const uint8_t* nvec, cudaStream_t s, GraphTables* gt);
+
+}  // namespace hb

@@ -1,0 +1,238 @@
+"""HEOM propagation API (drop-in for the reference heom.py).
+
+The hierarchy of auxiliary density operators (ADOs) sigma^(n) evolves as
+(heom.py:7-20, generalised to K Matsubara terms per site, modes m = (j, k))
+
+    d/dt sigma^n = -i[H, sigma^n] + L_markov(sigma^n) - (sum_m n_m nu_m) sigma^n
+                   + sum_m i [P_j(m), sigma^(n+e_m)] + sum_m n_m theta_m(sigma^(n-e_m))
+    theta_m = i a_k [P_j, .] + b_k {P_j, .}
+
+and is integrated with classical RK4.  Everything inside the time loop runs on
+the GPU (csrc/hb_stage.cu); this module validates inputs exactly like the
+reference, prepares operands (engine.BlockOperands), starts the device run and
+assembles the Trajectory.  Reference line numbers: PropagationConfig :57-94,
+propagate_from :286-406, propagate :409-419, auto_truncate :422-446.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .engine import (BlockOperands, DeviceRun, bath_coefficients, bath_modes,  # noqa: F401
+                     loss_channels)
+from .hierarchy import HierarchyGraph, hierarchy_size
+from .model import BathParams, ExcitonSystem, MarkovRates
+from .observables import Trajectory, trapping_time
+
+
+class PropagationDiverged(RuntimeError):
+    """A matrix norm exceeded the blow-up bound during time stepping."""
+
+
+class ConvergenceFailure(RuntimeError):
+    """A stop policy or truncation search did not converge within its cap."""
+
+
+@dataclass(frozen=True)
+class PropagationConfig:
+    """Time stepping and stop policy (reference fields and defaults) plus the
+    B200 options.
+
+    New fields (defaults reproduce the reference):
+      n_matsubara  K, Matsubara terms per site (0 = the reference's bath);
+      device       CUDA ordinal;
+      layout       'auto' (Hermitian-packed when rho0 is exactly Hermitian),
+                   'hermitian' or 'general';
+      ordering     device ADO order: 'lex' (locality) or 'reference';
+      chunk_steps  RK4 steps per CUDA-graph launch (0 = library default).
+    """
+
+    dt_fs: float = 2.5
+    n_max: int = 8
+    t_end_fs: Optional[float] = None
+    residual: Optional[float] = 1e-5
+    hard_cap_fs: float = 200_000.0
+    record_stride: int = 1
+    precision: str = "double"
+    record_matrices: bool = False
+    blowup_norm: float = 1e6
+    n_matsubara: int = 0
+    device: int = 0
+    layout: str = "auto"
+    ordering: str = "lex"
+    chunk_steps: int = 0
+
+    def __post_init__(self):
+        if self.dt_fs <= 0:
+            raise ValueError("dt must be > 0")
+        if self.n_max < 0:
+            raise ValueError("n_max must be >= 0")
+        if self.record_stride < 1:
+            raise ValueError("record stride must be >= 1")
+        if self.precision not in ("double", "single"):
+            raise ValueError("precision must be 'double' or 'single'")
+        if self.t_end_fs is None and self.residual is None:
+            raise ValueError("need a stop policy: t_end_fs or residual")
+        if self.t_end_fs is not None and self.t_end_fs < 0:
+            raise ValueError("t_end_fs must be >= 0")
+        if self.n_matsubara < 0:
+            raise ValueError("n_matsubara must be >= 0")
+        if self.layout not in N.HB_LAYOUT:
+            raise ValueError("layout must be 'auto', 'hermitian' or 'general'")
+        if self.ordering not in N.HB_ORDER:
+            raise ValueError("ordering must be 'lex' or 'reference'")
+
+    @property
+    def dtype(self):
+        return np.complex128 if self.precision == "double" else np.complex64
+
+
+@dataclass
+class HierarchyState:
+    """Full hierarchy state on the host (reference order): sigma[0] is rho."""
+
+    sigma: np.ndarray
+    time_fs: float = 0.0
+
+    @classmethod
+    def initial(cls, graph: HierarchyGraph, system: ExcitonSystem, rho0: np.ndarray,
+                dtype=np.complex128) -> "HierarchyState":
+        d = system.dimension
+        sigma = np.zeros((graph.n_tot, d, d), dtype=dtype)
+        sigma[0] = np.asarray(rho0, dtype=dtype)
+        return cls(sigma=sigma, time_fs=0.0)
+
+    @property
+    def rho(self) -> np.ndarray:
+        return self.sigma[0]
+
+
+def lindblad_markov(rho: np.ndarray, system: ExcitonSystem, rates: MarkovRates) -> np.ndarray:
+    """Sum over loss channels of D(V) rho = V rho V+ - {V+V, rho}/2 (heom.py:137-150)."""
+    out = np.zeros_like(rho, dtype=complex)
+    for rate, src, dst in loss_channels(system, rates):
+        out[dst, dst] += rate * rho[src, src]
+        out[src, :] -= 0.5 * rate * rho[src, :]
+        out[:, src] -= 0.5 * rate * rho[:, src]
+    return out
+
+
+def bath_backaction(system: ExcitonSystem, site_label: int, sigma: np.ndarray,
+                    bath: BathParams) -> np.ndarray:
+    """theta(sigma) = i a [P, sigma] + b {P, sigma} for one site (heom.py:153-165)."""
+    a, b = bath_coefficients(bath)
+    idx = system.site_basis_index(site_label)
+    out = np.zeros_like(sigma, dtype=complex)
+    out[idx, :] += (b + 1j * a) * sigma[idx, :]
+    out[:, idx] += (b - 1j * a) * sigma[:, idx]
+    return out
+
+
+def _check_rho0(system: ExcitonSystem, rho0) -> np.ndarray:
+    rho0 = np.asarray(rho0, dtype=complex)
+    d = system.dimension
+    if rho0.shape != (d, d):
+        raise ValueError(f"initial state must be {d}x{d}")
+    if not np.allclose(rho0, rho0.conj().T, atol=1e-12):
+        raise ValueError("initial state must be Hermitian")
+    return rho0
+
+
+def _graph_checks(n_sites: int, n_max: int) -> None:
+    # enumerate_hierarchy's validation (hierarchy.py:61-69), raised in the same order
+    if n_sites < 1:
+        raise ValueError("need at least one site")
+    if n_max < 0:
+        raise ValueError("truncation tier must be >= 0")
+    n_tot = hierarchy_size(n_sites, n_max)
+    if n_tot > np.iinfo(np.int32).max:
+        raise ValueError(f"hierarchy with {n_tot} indices exceeds the supported index range")
+
+
+def _trajectory(system, ops, config, run, steps, pops, mats, stop_reason) -> Trajectory:
+    sig0, sinks = run.sigma0()
+    d = system.dimension
+    final = np.zeros((d, d), dtype=complex)
+    final[np.ix_(ops.block, ops.block)] = sig0
+    for k, s in enumerate(ops.sinks):
+        final[s, s] = sinks[k]
+    return Trajectory(
+        times_fs=np.array([int(s) * config.dt_fs for s in steps]),
+        populations=pops,
+        site_indices=system.site_indices,
+        ground_index=system.ground_index,
+        rc_index=system.rc_index,
+        stop_reason=stop_reason,
+        final_rho=final,
+        residual_threshold=config.residual,
+        matrices=mats,
+    )
+
+
+def propagate_from(system: ExcitonSystem, bath: BathParams, rates: MarkovRates,
+                   config: PropagationConfig, rho0: np.ndarray) -> Trajectory:
+    """Propagate an arbitrary block-supported initial density matrix on the GPU."""
+    rho0 = _check_rho0(system, rho0)
+    K = config.n_matsubara
+    _graph_checks(system.site_count * (K + 1), config.n_max)
+    ops = BlockOperands(system, bath, rates, K)
+    d = system.dimension
+    for s in ops.sinks:
+        if any(rho0[s, j] != 0 for j in range(d) if j != s):  # row only, as heom.py:303-305
+            raise ValueError("initial state must not carry sink coherences")
+    if config.precision != "double":
+        raise NotImplementedError("precision='single' is not built yet (DESIGN.md, next rows)")
+    block = rho0[np.ix_(ops.block, ops.block)]
+    if config.layout == "hermitian" and not np.array_equal(block, block.conj().T):
+        raise ValueError("layout='hermitian' needs an exactly Hermitian rho0")
+    run = DeviceRun(ops, config.n_max, config.dt_fs, t_end_fs=config.t_end_fs,
+                    residual=config.residual, hard_cap_fs=config.hard_cap_fs,
+                    record_stride=config.record_stride, record_matrices=config.record_matrices,
+                    blowup_norm=config.blowup_norm, device=config.device, layout=config.layout,
+                    ordering=config.ordering, chunk_steps=config.chunk_steps)
+    with run:
+        run.set_rho0(block, [float(rho0[s, s].real) for s in ops.sinks])
+        rc = run.run()
+        if rc == N.HB_DIVERGED:
+            step = int(run.result.steps)
+            raise PropagationDiverged(
+                f"matrix norm exceeded {config.blowup_norm:g} at t = {step * config.dt_fs} fs")
+        if rc == N.HB_HARDCAP:
+            raise ConvergenceFailure(
+                f"residual policy not reached within the {config.hard_cap_fs} fs cap")
+        reason = {N.HB_STOP_T_END: "t_end", N.HB_STOP_RESIDUAL: "residual"}.get(
+            run.result.stop_reason)
+        steps, pops, mats = run.records()
+        return _trajectory(system, ops, config, run, steps, pops, mats, reason)
+
+
+def propagate(system: ExcitonSystem, bath: BathParams, rates: MarkovRates,
+              config: PropagationConfig, initial_site: int = 1) -> Trajectory:
+    """Propagate from |site><site| with all auxiliaries zero."""
+    idx = system.site_basis_index(initial_site)
+    rho0 = np.zeros((system.dimension, system.dimension), dtype=complex)
+    rho0[idx, idx] = 1.0
+    return propagate_from(system, bath, rates, config, rho0)
+
+
+def auto_truncate(system: ExcitonSystem, bath: BathParams, rates: MarkovRates,
+                  config: PropagationConfig, initial_site: int = 1, tol_ps: float = 0.02,
+                  start_n: int = 2, n_cap: int = 20) -> tuple:
+    """Raise n_max until consecutive trapping times agree within tol_ps."""
+    if tol_ps <= 0:
+        raise ValueError("tolerance must be > 0")
+    n = 0 if bath.lam_cm1 == 0 else max(0, start_n)
+    prev = propagate(system, bath, rates, replace(config, n_max=n), initial_site)
+    prev_t = trapping_time(prev)
+    while n < n_cap:
+        cur = propagate(system, bath, rates, replace(config, n_max=n + 1), initial_site)
+        cur_t = trapping_time(cur)
+        if abs(cur_t - prev_t) <= tol_ps:
+            return n, prev
+        n += 1
+        prev, prev_t = cur, cur_t
+    raise ConvergenceFailure(f"trapping time not converged to {tol_ps} ps by n_max = {n_cap}")

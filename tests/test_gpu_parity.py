@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle on the same inputs."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1012_4382_b200 as xf
+from oracle import oracle as orc
+from paper_1012_4382_b200 import _native as N
+from paper_1012_4382_b200.engine import BlockOperands, DeviceRun
+from tests.cases import BATH300, DIMER, FMO, RATES, TRAJ_CASES, site_rho
+
+pytestmark = pytest.mark.gpu
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------- tables (A1)
+
+def test_device_tables_bit_exact_small(golden_tables):
+    keys = sorted({k.rsplit("_", 1)[0] for k in golden_tables.files})
+    for key in keys:
+        m, n = (int(x[1:]) for x in key.split("_"))
+        g = xf.enumerate_hierarchy(m, n)
+        for name in ("indices", "tiers", "plus", "minus"):
+            arr = getattr(g, name)
+            assert arr.dtype == np.int32
+            assert np.array_equal(arr, golden_tables[f"{key}_{name}"]), (key, name)
+
+
+@pytest.mark.parametrize("key", ["M7_N6", "M7_N8", "M7_N10", "M14_N4", "M14_N6", "M14_N8"])
+def test_device_tables_bit_exact_hashed(golden_hashes, key):
+    m, n = (int(x[1:]) for x in key.split("_"))
+    ref = golden_hashes[key]
+    g = xf.enumerate_hierarchy(m, n)
+    assert g.n_tot == ref["n_tot"]
+    for name in ("indices", "tiers", "plus", "minus"):
+        assert _sha(getattr(g, name)) == ref[name], (key, name)
+
+
+def test_locality_permutation_is_lexicographic():
+    g = xf.enumerate_hierarchy(5, 4)
+    perm = np.asarray(g.perm)
+    assert sorted(perm.tolist()) == list(range(g.n_tot))
+    order = np.argsort(perm)
+    rows = [tuple(r) for r in g.indices[order]]
+    assert rows == sorted(rows)          # device order = pure lexicographic
+    assert perm[0] == 0                  # the root stays first
+
+
+def test_index_of_and_errors():
+    g = xf.enumerate_hierarchy(7, 3)
+    for k in range(g.n_tot):
+        assert xf.index_of(g, g.indices[k]) == k
+    with pytest.raises(KeyError):
+        xf.index_of(g, (4, 0, 0, 0, 0, 0, 0))
+    with pytest.raises(ValueError):
+        xf.enumerate_hierarchy(64, 64)
+    with pytest.raises(ValueError):
+        xf.enumerate_hierarchy(0, 4)
+
+
+# ------------------------------------------------- Level-2 kernel ABI (A3-A6)
+
+@pytest.mark.parametrize("case", ["fmo_n2", "fmo_n3_77k", "dimer_n4", "dephasing_n5"])
+def test_rhs_shim_matches_reference_kernel(golden_rhs, case):
+    from paper_1012_4382_b200 import kernels
+    g = golden_rhs
+    n_sites, n_max = int(g[case + "_n_sites"]), int(g[case + "_n_max"])
+    graph = xf.enumerate_hierarchy(n_sites, n_max)
+    sig = g[case + "_sig"]
+    out = np.empty_like(sig)
+    kernels.hierarchy_rhs_kernel(out, sig, g[case + "_h"], g[case + "_site_of"], graph.plus,
+                                 graph.minus, graph.indices.astype(np.float64),
+                                 graph.tiers * float(g[case + "_gamma"]), float(g[case + "_a"]),
+                                 float(g[case + "_b"]), g[case + "_decay"])
+    ref = g[case + "_out"]
+    assert np.max(np.abs(out - ref)) <= 1e-14 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("case", ["fmo_n2", "dimer_n4"])
+def test_elementwise_shims(golden_rhs, case):
+    from paper_1012_4382_b200 import kernels
+    g = golden_rhs
+    x = g[case + "_sig"].reshape(-1).copy()
+    y = g[case + "_out"].reshape(-1).copy()
+    tmp = np.empty_like(x)
+    kernels.add_scaled(tmp, x, y, 0.37)
+    assert np.max(np.abs(tmp - g[case + "_add_scaled"])) <= 1e-15 * np.max(np.abs(tmp))
+    s2 = x.copy()
+    kernels.rk4_update(s2, x, y, tmp, x[::-1].copy(), 0.125)
+    assert np.max(np.abs(s2 - g[case + "_rk4_update"])) <= 1e-15 * np.max(np.abs(s2))
+    assert kernels.max_abs2(y) == float(g[case + "_max_abs2"])
+
+
+# ------------------------------------------------------- propagation (A7-A10)
+
+@pytest.mark.parametrize("name", list(TRAJ_CASES))
+def test_trajectory_matches_reference(golden_traj, name):
+    arrays, meta = golden_traj
+    system, bath, rates, kw, rho0 = TRAJ_CASES[name]
+    traj = xf.propagate_from(system, bath, rates, xf.PropagationConfig(**kw), rho0)
+    assert traj.stop_reason == meta[name]["stop_reason"]
+    assert np.array_equal(traj.times_fs, arrays[name + "_times"])
+    assert np.max(np.abs(traj.populations - arrays[name + "_pops"])) < 1e-10
+    assert np.max(np.abs(traj.final_rho - arrays[name + "_final_rho"])) < 1e-10
+    if name + "_matrices" in arrays.files:
+        assert np.max(np.abs(traj.matrices - arrays[name + "_matrices"])) < 1e-10
+
+
+def test_efficiency_and_trapping_time(golden_traj):
+    arrays, meta = golden_traj
+    system, bath, rates, kw, rho0 = TRAJ_CASES["fmo_n2_eta"]
+    traj = xf.propagate_from(system, bath, rates, xf.PropagationConfig(**kw), rho0)
+    assert abs(xf.efficiency(traj) - meta["fmo_n2_eta"]["eta"]) < 1e-10
+    assert abs(xf.trapping_time(traj) - meta["fmo_n2_eta"]["trapping_time_ps"]) < 1e-8
+    assert abs(xf.efficiency(traj) + traj.ground_population()[-1] - 1.0) < 1e-5
+
+
+def test_divergence_guard_message(golden_traj):
+    _, meta = golden_traj
+    cfg = xf.PropagationConfig(dt_fs=150.0, n_max=2, t_end_fs=30000.0, residual=None)
+    with pytest.raises(xf.PropagationDiverged) as exc:
+        xf.propagate(FMO, BATH300, RATES, cfg, 1)
+    assert str(exc.value) == meta["diverge"]["message"]
+
+
+def test_hard_cap_message(golden_traj):
+    _, meta = golden_traj
+    cfg = xf.PropagationConfig(dt_fs=2.5, n_max=0, residual=1e-5, hard_cap_fs=500.0)
+    with pytest.raises(xf.ConvergenceFailure) as exc:
+        xf.propagate(FMO, BATH300, xf.MarkovRates.none(), cfg, 1)
+    assert str(exc.value) == meta["hardcap"]["message"]
+
+
+def test_layouts_and_orderings_agree():
+    base = dict(dt_fs=2.5, n_max=3, t_end_fs=300.0, residual=None)
+    ref = xf.propagate(FMO, BATH300, RATES, xf.PropagationConfig(**base), 1).populations
+    for layout in ("hermitian", "general"):
+        for ordering in ("lex", "reference"):
+            cfg = xf.PropagationConfig(**base, layout=layout, ordering=ordering)
+            p = xf.propagate(FMO, BATH300, RATES, cfg, 1).populations
+            assert np.max(np.abs(p - ref)) < 1e-13, (layout, ordering)
+
+
+def test_chunking_does_not_change_results():
+    base = dict(dt_fs=5.0, n_max=2, residual=1e-5, record_stride=3)
+    a = xf.propagate(FMO, BATH300, RATES, xf.PropagationConfig(**base, chunk_steps=1), 1)
+    b = xf.propagate(FMO, BATH300, RATES, xf.PropagationConfig(**base, chunk_steps=97), 1)
+    assert np.array_equal(a.times_fs, b.times_fs)
+    assert np.array_equal(a.populations, b.populations)
+
+
+def test_zero_truncation_equals_markov_only():
+    cfg = xf.PropagationConfig(dt_fs=1.0, n_max=0, t_end_fs=200.0, residual=None)
+    a = xf.propagate(FMO, BATH300, RATES, cfg, 1).populations
+    b = xf.propagate(FMO, xf.BathParams.from_timescale(0.0, 166.0, 300.0), RATES, cfg, 1).populations
+    assert np.max(np.abs(a - b)) == 0.0
+
+
+def test_t_end_zero_and_initial_residual():
+    cfg = xf.PropagationConfig(dt_fs=2.5, n_max=2, t_end_fs=0.0, residual=None)
+    traj = xf.propagate(FMO, BATH300, RATES, cfg, 1)
+    assert traj.times_fs.tolist() == [0.0] and traj.stop_reason == "t_end"
+    rho0 = np.zeros((9, 9), complex)
+    rho0[8, 8] = 1.0  # everything already trapped
+    traj = xf.propagate_from(FMO, BATH300, RATES, xf.PropagationConfig(dt_fs=2.5, n_max=2), rho0)
+    assert traj.stop_reason == "residual" and len(traj.times_fs) == 1
+
+
+def test_input_validation():
+    cfg = xf.PropagationConfig(dt_fs=2.5, n_max=0, t_end_fs=10.0, residual=None)
+    bad = site_rho(1)
+    bad[0, 1] = bad[1, 0] = 0.1
+    with pytest.raises(ValueError):
+        xf.propagate_from(FMO, BATH300, RATES, cfg, bad)
+    with pytest.raises(ValueError):
+        xf.propagate(FMO, BATH300, RATES, cfg, 8)
+    with pytest.raises(ValueError):
+        xf.propagate_from(FMO, BATH300, RATES, cfg, np.eye(3))
+
+
+# --------------------------------------------------------- K >= 1 (unpinned)
+
+@pytest.mark.parametrize("n_max", [2, 3])
+def test_matsubara_k1_matches_oracle(n_max):
+    cfg = xf.PropagationConfig(dt_fs=1.0, n_max=n_max, t_end_fs=150.0, residual=None,
+                               n_matsubara=1, record_stride=5)
+    traj = xf.propagate(FMO, BATH300, RATES, cfg, 1)
+    ref = orc.propagate_from(FMO, BATH300, RATES, cfg, site_rho(1))
+    assert np.max(np.abs(traj.populations - ref["populations"])) < 1e-10
+    assert np.max(np.abs(traj.final_rho - ref["final_rho"])) < 1e-10
+
+
+def test_matsubara_zero_coefficient_equals_k0():
+    bath = xf.BathParams.from_timescale(20.0, 100.0, 77.0)
+    nu, a, b = xf.bath_modes(bath, 0)
+    ops0 = BlockOperands(DIMER, bath, xf.MarkovRates.none(), 0)
+    ops1 = BlockOperands(DIMER, bath, xf.MarkovRates.none(), 1,
+                         modes=(np.array([nu[0], 3.0]), np.array([a[0], 0.0]), np.array([b[0], 0.0])))
+    out = []
+    for ops in (ops0, ops1):
+        with DeviceRun(ops, 3, 0.5, t_end_fs=200.0) as run:
+            run.set_rho0(np.diag([1.0, 0.0]).astype(complex), [])
+            assert run.run() == N.HB_OK
+            out.append(run.records()[1])
+    assert np.max(np.abs(out[0] - out[1])) < 1e-15
+
+
+@pytest.mark.slow
+def test_long_eta_twin(golden_long):
+    arrays, meta = golden_long
+    cfg = xf.PropagationConfig(dt_fs=2.5, n_max=6, residual=1e-5, record_stride=100)
+    traj = xf.propagate(FMO, BATH300, RATES, cfg, 1)
+    m = meta["fmo_n6_eta"]
+    assert traj.stop_reason == "residual"
+    assert np.array_equal(traj.times_fs, arrays["fmo_n6_eta_times"])
+    assert np.max(np.abs(traj.populations - arrays["fmo_n6_eta_pops"])) < 1e-10
+    assert abs(xf.efficiency(traj) - m["eta"]) < 1e-10
+
+
+def test_large_hierarchy_two_steps_vs_oracle():
+    """Config 4 shape (FMO 300 K, N_max=8, K=1, 319,770 ADOs): two RK4 steps."""
+    cfg = xf.PropagationConfig(dt_fs=1.0, n_max=8, t_end_fs=2.0, residual=None, n_matsubara=1)
+    traj = xf.propagate(FMO, BATH300, RATES, cfg, 1)
+    orc.set_threads(8)
+    ref = orc.propagate_from(FMO, BATH300, RATES, cfg, site_rho(1))
+    orc.set_threads(1)
+    assert np.max(np.abs(traj.populations - ref["populations"])) < 1e-12
+    assert np.max(np.abs(traj.final_rho - ref["final_rho"])) < 1e-12
