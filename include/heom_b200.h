@@ -43,6 +43,10 @@ extern "C" {
 #define HB_ORDER_LEX 0         /* pure lexicographic over all tiers (locality)  */
 #define HB_ORDER_REFERENCE 1   /* tier-major lexicographic (hierarchy.py:71-78) */
 
+/* stage-kernel variants */
+#define HB_KERNEL_AUTO 0       /* unrolled thread-per-ADO kernel when the shape allows */
+#define HB_KERNEL_GENERIC 1    /* runtime-shaped tile kernel (any d, K, layout)        */
+
 #define HB_MAX_D 8
 #define HB_MAX_KP1 8
 #define HB_MAX_SINKS 4
@@ -83,6 +87,7 @@ typedef struct {
     int layout;               /* HB_LAYOUT_*                                      */
     int ordering;             /* HB_ORDER_*                                       */
     int chunk_steps;          /* RK4 steps per CUDA-graph launch (0 = default)    */
+    int kernel_variant;       /* HB_KERNEL_*                                      */
 } hb_params;
 
 typedef struct {

@@ -7,9 +7,14 @@
 // graph and synchronises once per chunk to drain records and read the status
 // written by the last CTA of each stage-4 kernel (hb_stage.cu).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 #include "hb_internal.h"
 
@@ -31,6 +36,52 @@ static int cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
   } while (0)
 
+// Device hierarchy tables are immutable, so handles with the same
+// (modes, n_max, ordering, device) share one copy -- the analogue of the
+// reference's lru_cache'd _graph (heom.py:222-224).
+namespace {
+using GraphKey = std::tuple<int, int, int, int>;
+struct CachedGraph {
+  GraphTables gt;
+  ~CachedGraph() { free_graph(&gt); }
+};
+std::mutex g_graph_mu;
+std::map<GraphKey, std::shared_ptr<CachedGraph>> g_graphs;  // LRU of 8, like lru_cache(8)
+std::vector<GraphKey> g_graph_lru;
+
+cudaError_t shared_graph(int modes, int n_max, int ordering, int device, cudaStream_t s,
+                         std::shared_ptr<CachedGraph>* out) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  const GraphKey key{modes, n_max, ordering, device};
+  auto touch = [&] {
+    for (size_t i = 0; i < g_graph_lru.size(); ++i)
+      if (g_graph_lru[i] == key) {
+        g_graph_lru.erase(g_graph_lru.begin() + i);
+        break;
+      }
+    g_graph_lru.push_back(key);
+  };
+  auto it = g_graphs.find(key);
+  if (it != g_graphs.end()) {
+    *out = it->second;
+    touch();
+    return cudaSuccess;
+  }
+  auto sp = std::make_shared<CachedGraph>();
+  cudaError_t e = build_graph(modes, n_max, ordering, s, nullptr, nullptr, nullptr, nullptr,
+                              nullptr, &sp->gt);
+  if (e != cudaSuccess) return e;
+  g_graphs[key] = sp;
+  touch();
+  while (g_graph_lru.size() > 8) {  // handles still using an evicted graph keep it alive
+    g_graphs.erase(g_graph_lru.front());
+    g_graph_lru.erase(g_graph_lru.begin());
+  }
+  *out = sp;
+  return cudaSuccess;
+}
+}  // namespace
+
 struct hb_handle {
   hb_params prm{};
   std::vector<double> h, decay, nu, a, b, sink_rate;
@@ -39,10 +90,12 @@ struct hb_handle {
   int modes = 0, n_tot = 0, n_tiles = 0;
   int chunk = 64;
   cudaStream_t stream = nullptr;
-  GraphTables gt;
+  std::shared_ptr<CachedGraph> graph_ref;  // shared device tables
+  GraphTables gt;                          // copy of graph_ref->gt (non-owning)
   int layout = 0;  // HB_LAYOUT_HERMITIAN / GENERAL once allocated
   int n_planes = 0;
   double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // sigma, Y2, Y3, Y4
+  double* zero_tile = nullptr;  // never written: target of absent links
   Ctl* ctl = nullptr;
   Ctl* ctl_host = nullptr;  // pinned
   long long* rec_step = nullptr;
@@ -257,7 +310,7 @@ void hb_destroy(hb_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_state(h);
-  free_graph(&h->gt);
+  h->graph_ref.reset();
   cudaFree(h->ctl);
   cudaFreeHost(h->ctl_host);
   cudaFree(h->rec_step);
@@ -277,6 +330,7 @@ int hb_create(const hb_params* P, hb_handle** out) {
   if (q.n_sinks < 0 || q.n_sinks > MAXS) return fail(HB_ERR_ARG, "too many sinks");
   if (q.n_site_pos < 0 || q.n_site_pos > MAXD) return fail(HB_ERR_ARG, "bad site positions");
   if (q.d_full < q.d) return fail(HB_ERR_ARG, "d_full < d");
+  if (q.d_full > MAXFULL) return fail(HB_ERR_ARG, "full basis dimension above 16 is not supported");
   if (!(q.dt > 0)) return fail(HB_ERR_ARG, "dt must be > 0");
   if (q.record_stride < 1) return fail(HB_ERR_ARG, "record stride must be >= 1");
   int nterms = 0;
@@ -320,12 +374,16 @@ int hb_create(const hb_params* P, hb_handle** out) {
   if (e) return bail(e, "cudaSetDevice");
   e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
   if (e) return bail(e, "cudaStreamCreate");
-  e = build_graph(modes, q.n_max, q.ordering, h->stream, nullptr, nullptr, nullptr, nullptr,
-                  nullptr, &h->gt);
+  e = shared_graph(modes, q.n_max, q.ordering, h->device, h->stream, &h->graph_ref);
   if (e) return bail(e, "build_graph");
+  h->gt = h->graph_ref->gt;
   h->n_tiles = h->gt.n_tiles;
   e = cudaMalloc(&h->ctl, sizeof(Ctl));
   if (e) return bail(e, "cudaMalloc(ctl)");
+  const size_t zbytes = (size_t)2 * MAXD * MAXD * TILE * sizeof(double);
+  e = cudaMalloc(&h->zero_tile, zbytes);
+  if (!e) e = cudaMemsetAsync(h->zero_tile, 0, zbytes, h->stream);
+  if (e) return bail(e, "cudaMalloc(zero tile)");
   e = cudaMallocHost(&h->ctl_host, sizeof(Ctl));
   if (e) return bail(e, "cudaMallocHost(ctl)");
   h->rec_cap = h->chunk + 4;
@@ -342,6 +400,7 @@ int hb_create(const hb_params* P, hb_handle** out) {
   p.modes = modes;
   p.n_tot = h->n_tot;
   p.n_tiles = h->n_tiles;
+  p.n_tiles_total = h->n_tiles;
   p.tile_begin = 0;
   for (int i = 0; i < d; ++i) {
     for (int j = 0; j < d; ++j) p.h[i * MAXD + j] = h->h[i * d + j];
@@ -358,6 +417,15 @@ int hb_create(const hb_params* P, hb_handle** out) {
   p.minus = h->gt.minus_t;
   p.nvec = h->gt.nvec_t;
   p.damp_plane = nullptr;
+  p.zero_tile = h->zero_tile;
+  {
+    const char* e = getenv("HB_PREFETCH");
+    p.prefetch = e ? atoi(e) : 1;
+    const char* g = getenv("HB_DEBUG_NOGATHER");
+    p.debug = g ? atoi(g) : 0;
+    const char* d = getenv("HB_PFD");
+    p.pf_dist = d ? atoi(d) : 0;
+  }
   p.dt = q.dt;
   p.ctl = h->ctl;
   p.n_sinks = q.n_sinks;
@@ -372,6 +440,9 @@ int hb_create(const hb_params* P, hb_handle** out) {
   p.n_site_pos = q.n_site_pos;
   for (int k = 0; k < q.n_site_pos; ++k) p.site_pos[k] = h->site_pos[k];
   p.d_full = q.d_full;
+  for (int f = 0; f < MAXFULL; ++f) p.full2blk[f] = p.full2sink[f] = -1;
+  for (int i = 0; i < d; ++i) p.full2blk[h->block_full[i]] = i;
+  for (int s = 0; s < q.n_sinks; ++s) p.full2sink[h->sink_full[s]] = s;
   p.has_t_end = q.has_t_end;
   p.has_residual = q.has_residual;
   p.record_matrices = q.record_matrices;
@@ -413,13 +484,19 @@ static int alloc_state(hb_handle* h, int layout) {
   h->layout = layout;
   const int d = h->prm.d;
   h->n_planes = layout == HB_LAYOUT_HERMITIAN ? d * d : 2 * d * d;
-  const size_t bytes = (size_t)h->n_tiles * TILE * h->n_planes * sizeof(double);
+  // one extra all-zero tile per buffer: target of absent links (never written)
+  const size_t bytes = (size_t)(h->n_tiles + 1) * TILE * h->n_planes * sizeof(double);
   for (auto& b : h->buf) {
     CK(cudaMalloc(&b, bytes));
     CK(cudaMemsetAsync(b, 0, bytes, h->stream));
   }
   h->base.hermitian = layout == HB_LAYOUT_HERMITIAN;
   h->base.n_planes = h->n_planes;
+  bool identity = h->prm.n_sites == d;
+  for (int i = 0; i < d; ++i) identity = identity && h->site_of[i] == i;
+  h->base.fast = h->base.hermitian && identity && fast_supported(d, h->prm.kp1) &&
+                 h->prm.kernel_variant == HB_KERNEL_AUTO;
+  if (h->base.fast) CK(configure_fast(h->base));
   CK(configure_stages(h->base));
   return HB_OK;
 }

@@ -1,0 +1,256 @@
+// Device-side helpers shared by the stage kernels (hb_stage.cu, hb_fast.cu):
+// packed-plane bookkeeping, numpy-compatible summation and the scalar per-step
+// bookkeeping done by the last CTA of a stage-4 launch (sinks, guard, records,
+// stop policy -- heom.py:355-394).
+#pragma once
+#include "hb_internal.h"
+
+namespace hb {
+
+template <int D, bool HERM>
+struct Lay {
+  static constexpr int NP = HERM ? D * D : 2 * D * D;      // float64 planes per ADO
+  static constexpr int NE = HERM ? D * (D + 1) / 2 : D * D;  // elements per ADO
+};
+
+// element e -> (i, j) and its planes; Hermitian: e < D diagonal (real),
+// then the upper triangle row-major.
+template <int D, bool HERM>
+__device__ __forceinline__ void elem_info(int e, int& i, int& j, int& pr, int& pim) {
+  if (HERM) {
+    if (e < D) {
+      i = j = e;
+      pr = e;
+      pim = -1;
+      return;
+    }
+    int o = e - D, r = 0, cnt = D - 1;
+    while (o >= cnt) {
+      o -= cnt;
+      ++r;
+      cnt = D - 1 - r;
+    }
+    i = r;
+    j = r + 1 + o;
+    pr = D + 2 * (e - D);
+    pim = pr + 1;
+  } else {
+    i = e / D;
+    j = e % D;
+    pr = 2 * e;
+    pim = 2 * e + 1;
+  }
+}
+
+// plane p -> (i, j, part) for the unpack into shared memory
+template <int D, bool HERM>
+__device__ __forceinline__ void plane_info(int p, int& i, int& j, int& part) {
+  if (HERM) {
+    if (p < D) {
+      i = j = p;
+      part = 0;
+      return;
+    }
+    int e = D + ((p - D) >> 1);
+    int pr, pim;
+    elem_info<D, HERM>(e, i, j, pr, pim);
+    part = (p - D) & 1;
+  } else {
+    const int e = p >> 1;
+    i = e / D;
+    j = e % D;
+    part = p & 1;
+  }
+}
+
+// sigma^0 entry (i, j) straight from global memory (tile 0, lane 0)
+template <int D, bool HERM>
+__device__ __forceinline__ void load_sig0(const double* s, int i, int j, double& re, double& im) {
+  if (HERM) {
+    if (i == j) {
+      re = __ldcg(s + i * TILE);
+      im = 0.0;
+      return;
+    }
+    const int a = i < j ? i : j, b = i < j ? j : i;
+    int e = D;
+    for (int r = 0; r < a; ++r) e += D - 1 - r;
+    e += b - a - 1;
+    const int pr = D + 2 * (e - D);
+    re = __ldcg(s + pr * TILE);
+    im = __ldcg(s + (pr + 1) * TILE);
+    if (i > j) im = -im;
+  } else {
+    const int e = i * D + j;
+    re = __ldcg(s + 2 * e * TILE);
+    im = __ldcg(s + (2 * e + 1) * TILE);
+  }
+}
+
+// TMA bulk prefetch of a contiguous range into L2 (no registers, no smem);
+// 16-byte aligned, size a multiple of 16
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// epilogue operands of a stage (sigma; + Y2, Y3 at stage 4) for one tile
+template <int STAGE>
+__device__ __forceinline__ void prefetch_epilogue(const KParams& P, size_t tile_off, unsigned bytes) {
+  if (STAGE >= 2) prefetch_l2(P.sig + tile_off, bytes);
+  if (STAGE == 4) {
+    prefetch_l2(P.Y2 + tile_off, bytes);
+    prefetch_l2(P.Y3 + tile_off, bytes);
+  }
+}
+
+// everything a stage reads for one tile except the gathers: own input, link
+// tables, epilogue operands -- bulk-prefetched into L2 one wave ahead
+template <int STAGE>
+__device__ __forceinline__ void prefetch_tile(const KParams& P, int tile) {
+  if (tile >= P.tile_begin + P.n_tiles) return;
+  const unsigned tbytes = (unsigned)(P.n_planes * TILE * sizeof(double));
+  const size_t off = (size_t)tile * P.n_planes * TILE;
+  prefetch_l2(P.Yin + off, tbytes);
+  prefetch_epilogue<STAGE>(P, off, tbytes);
+  const size_t goff = (size_t)tile * P.modes * TILE;
+  prefetch_l2(P.plus + goff, P.modes * TILE * 4);
+  prefetch_l2(P.minus + goff, P.modes * TILE * 4);
+  if ((P.modes * TILE) % 16 == 0) prefetch_l2(P.nvec + goff, P.modes * TILE);
+}
+
+// numpy add.reduce of a short float64 vector (pairwise_sum), see or_np_sum
+__device__ inline double np_sum(const double* x, int m) {
+  double rest;
+  if (m < 8) {
+    rest = -0.0;
+    for (int i = 0; i < m; ++i) rest += x[i];
+  } else {
+    double r[8];
+    for (int jj = 0; jj < 8; ++jj) r[jj] = x[jj];
+    int i;
+    for (i = 8; i < m - (m % 8); i += 8)
+      for (int jj = 0; jj < 8; ++jj) r[jj] += x[i + jj];
+    rest = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < m; ++i) rest += x[i];
+  }
+  return rest;
+}
+
+// ---------------------------------------------------------------------------
+// per-step bookkeeping, done by ONE WARP of the last CTA of a stage-4 launch
+// (and by the init kernel): sigma^0 is fetched once, in parallel, into shared
+// memory; records, guard and stop policy read it from there.
+
+struct Sig0 {
+  double re[MAXD * MAXD];
+  double im[MAXD * MAXD];
+};
+
+template <int D, bool HERM>
+__device__ void sig0_warp(const KParams& P, Sig0& s0) {
+  const int lane = threadIdx.x & 31;
+  for (int f = lane; f < D * D; f += 32) load_sig0<D, HERM>(P.sig, f / D, f % D, s0.re[f], s0.im[f]);
+  __syncwarp();
+}
+
+template <int D>
+__device__ void record_warp(const KParams& P, long long step, const Sig0& s0) {
+  const int lane = threadIdx.x & 31;
+  volatile Ctl* c = P.ctl;
+  const long long idx = c->n_rec;
+  if (idx >= P.rec_cap) return;  // host sizes the buffer for a whole chunk
+  const int df = P.d_full;
+  double* pops = P.rec_pops + idx * df;
+  for (int f = lane; f < df; f += 32) {
+    const int b = P.full2blk[f], sk = P.full2sink[f];
+    pops[f] = b >= 0 ? s0.re[b * D + b] : (sk >= 0 ? c->sink_pops[sk] : 0.0);
+  }
+  if (P.record_matrices) {
+    double* m = P.rec_mats + idx * df * df * 2;
+    for (int f = lane; f < df * df; f += 32) {
+      const int fi = f / df, fj = f % df;
+      const int bi = P.full2blk[fi], bj = P.full2blk[fj];
+      double re = 0.0, im = 0.0;
+      if (bi >= 0 && bj >= 0) {
+        re = s0.re[bi * D + bj];
+        im = s0.im[bi * D + bj];
+      } else if (fi == fj && P.full2sink[fi] >= 0) {
+        re = c->sink_pops[P.full2sink[fi]];
+      }
+      m[2 * f] = re;
+      m[2 * f + 1] = im;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    P.rec_step[idx] = step;
+    c->n_rec = idx + 1;
+  }
+  __syncwarp();
+}
+
+// stop policy evaluated before step `step` (heom.py:359-368)
+template <int D>
+__device__ void check_stop_warp(const KParams& P, long long step, const Sig0& s0) {
+  const int lane = threadIdx.x & 31;
+  volatile Ctl* c = P.ctl;
+  int st = ST_RUNNING;
+  if (lane == 0) {
+    const double t = (double)step * P.dt;
+    if (P.has_t_end && t >= P.t_end - 1e-9) {
+      st = ST_T_END;
+    } else if (P.has_residual) {
+      double diag[MAXD];
+      for (int k = 0; k < P.n_site_pos; ++k) diag[k] = s0.re[P.site_pos[k] * (D + 1)];
+      if (np_sum(diag, P.n_site_pos) <= P.residual) st = ST_RESIDUAL;
+    }
+    if (st == ST_RUNNING && !P.has_t_end && t >= P.hard_cap) st = ST_HARDCAP;
+  }
+  st = __shfl_sync(0xffffffffu, st, 0);
+  if (st == ST_RUNNING) return;
+  if (st != ST_HARDCAP && step % P.stride != 0) record_warp<D>(P, step, s0);
+  if (lane == 0) c->status = st;
+}
+
+template <int D, bool HERM>
+__device__ void finish_step_warp(const KParams& P, long long step) {
+  __shared__ Sig0 s0;
+  const int lane = threadIdx.x & 31;
+  volatile Ctl* c = P.ctl;
+  sig0_warp<D, HERM>(P, s0);
+  double m0 = 0.0;
+  for (int f = lane; f < D * D; f += 32) m0 = fmax(m0, s0.re[f] * s0.re[f] + s0.im[f] * s0.im[f]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+  int diverged = 0;
+  if (lane == 0) {
+    c->blocks_done = 0;
+    c->step = step;
+    for (int s = 0; s < P.n_sinks; ++s)
+      c->sink_pops[s] += (P.dt / 6.0) * (c->r[0][s] + 2.0 * (c->r[1][s] + c->r[2][s]) + c->r[3][s]);
+    const bool full = step % 25 == 0;
+    double mall = 0.0;
+    if (full) {
+      mall = __longlong_as_double((long long)c->maxabs2_bits);
+      c->maxabs2_bits = 0ull;
+    }
+    diverged = (m0 > P.blow2 || (full && mall > P.blow2));
+    if (diverged) c->status = ST_DIVERGED;
+  }
+  diverged = __shfl_sync(0xffffffffu, diverged, 0);
+  __syncwarp();
+  if (diverged) return;
+  if (step % P.stride == 0) record_warp<D>(P, step, s0);
+  check_stop_warp<D>(P, step, s0);
+}
+
+// t = 0 sample + stop policy before the first step (heom.py:355-368); 1 warp
+template <int D, bool HERM>
+__device__ void init_warp(const KParams& P) {
+  __shared__ Sig0 s0;
+  sig0_warp<D, HERM>(P, s0);
+  record_warp<D>(P, 0, s0);
+  check_stop_warp<D>(P, 0, s0);
+}
+
+}  // namespace hb

@@ -12,6 +12,7 @@ constexpr int MAXKP1 = HB_MAX_KP1;
 constexpr int MAXS = HB_MAX_SINKS;
 constexpr int MAXT = HB_MAX_SINK_TERMS;
 constexpr int MAX_MODES = 64;
+constexpr int MAXFULL = 16;       // full basis (block + sinks) for records
 
 enum Status : int {
   ST_RUNNING = 0,
@@ -44,6 +45,7 @@ struct KParams {
   double nu[MAXKP1], a[MAXKP1], b[MAXKP1];
   int d, n_sites, kp1, modes;
   int n_tot, n_tiles, tile_begin, n_planes;
+  int n_tiles_total;     // tiles per state buffer (a zero tile follows the last one)
   // state (AoSoA: [tile][plane][32] doubles)
   const double* Yin;     // stage input: own tile + gathers
   const double* sig;     // sigma (stages 2-4)
@@ -55,6 +57,11 @@ struct KParams {
   const int32_t* minus;
   const uint8_t* nvec;
   const double* damp_plane;  // optional per-ADO damping (Level-2 shim), else null
+  const double* zero_tile;   // NP*32 zeros: target of absent links (fast kernel)
+  int fast;                  // use the unrolled thread-per-ADO kernel (hb_fast.cu)
+  int prefetch;              // bulk-prefetch epilogue tiles into L2 at kernel start
+  int pf_dist;               // L2 prefetch distance in tiles (0 = off)
+  int debug;                 // timing experiments only (HB_DEBUG_NOGATHER): links -> zero tile
   double coef;               // dt/2, dt/2, dt for stages 1-3
   double dt;
   // bookkeeping
@@ -68,6 +75,8 @@ struct KParams {
   int d_full;
   int block_full[MAXD];
   int sink_full[MAXS];
+  int full2blk[MAXFULL];     // full index -> block position or -1
+  int full2sink[MAXFULL];    // full index -> sink slot or -1
   int has_t_end, has_residual, record_matrices, hermitian;
   double t_end, residual, hard_cap, blow2;
   long long stride;
@@ -76,6 +85,12 @@ struct KParams {
   double* rec_pops;
   double* rec_mats;
 };
+
+// hb_fast.cu: unrolled thread-per-ADO kernels for the production shape
+// (Hermitian layout, every block level is a site with site_of == identity)
+bool fast_supported(int d, int kp1);
+cudaError_t launch_fast(int stage, const KParams& p, cudaStream_t s);
+cudaError_t configure_fast(const KParams& p);  // before graph capture
 
 // hb_stage.cu
 cudaError_t launch_stage(int stage, const KParams& p, cudaStream_t s);

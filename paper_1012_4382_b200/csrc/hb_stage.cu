@@ -31,201 +31,9 @@
 // commutator needs a full row and column), the 2*modes neighbour links of the
 // tile are staged too; neighbour elements are gathered with read-only loads
 // (the neighbour maps are monotone so a warp's 32 gathers touch few sectors).
-#include "hb_internal.h"
+#include "hb_device.cuh"
 
 namespace hb {
-
-template <int D, bool HERM>
-struct Lay {
-  static constexpr int NP = HERM ? D * D : 2 * D * D;      // float64 planes per ADO
-  static constexpr int NE = HERM ? D * (D + 1) / 2 : D * D;  // elements per ADO
-};
-
-// element e -> (i, j) and its planes; Hermitian: e < D diagonal (real),
-// then the upper triangle row-major.
-template <int D, bool HERM>
-__device__ __forceinline__ void elem_info(int e, int& i, int& j, int& pr, int& pim) {
-  if (HERM) {
-    if (e < D) {
-      i = j = e;
-      pr = e;
-      pim = -1;
-      return;
-    }
-    int o = e - D, r = 0, cnt = D - 1;
-    while (o >= cnt) {
-      o -= cnt;
-      ++r;
-      cnt = D - 1 - r;
-    }
-    i = r;
-    j = r + 1 + o;
-    pr = D + 2 * (e - D);
-    pim = pr + 1;
-  } else {
-    i = e / D;
-    j = e % D;
-    pr = 2 * e;
-    pim = 2 * e + 1;
-  }
-}
-
-// plane p -> (i, j, part) for the unpack into shared memory
-template <int D, bool HERM>
-__device__ __forceinline__ void plane_info(int p, int& i, int& j, int& part) {
-  if (HERM) {
-    if (p < D) {
-      i = j = p;
-      part = 0;
-      return;
-    }
-    int e = D + ((p - D) >> 1);
-    int pr, pim;
-    elem_info<D, HERM>(e, i, j, pr, pim);
-    part = (p - D) & 1;
-  } else {
-    const int e = p >> 1;
-    i = e / D;
-    j = e % D;
-    part = p & 1;
-  }
-}
-
-// sigma^0 entry (i, j) straight from global memory (tile 0, lane 0)
-template <int D, bool HERM>
-__device__ __forceinline__ void load_sig0(const double* s, int i, int j, double& re, double& im) {
-  if (HERM) {
-    if (i == j) {
-      re = __ldcg(s + i * TILE);
-      im = 0.0;
-      return;
-    }
-    const int a = i < j ? i : j, b = i < j ? j : i;
-    int e = D;
-    for (int r = 0; r < a; ++r) e += D - 1 - r;
-    e += b - a - 1;
-    const int pr = D + 2 * (e - D);
-    re = __ldcg(s + pr * TILE);
-    im = __ldcg(s + (pr + 1) * TILE);
-    if (i > j) im = -im;
-  } else {
-    const int e = i * D + j;
-    re = __ldcg(s + 2 * e * TILE);
-    im = __ldcg(s + (2 * e + 1) * TILE);
-  }
-}
-
-// numpy add.reduce of a short float64 vector (pairwise_sum), see or_np_sum
-__device__ double np_sum(const double* x, int m) {
-  double rest;
-  if (m < 8) {
-    rest = -0.0;
-    for (int i = 0; i < m; ++i) rest += x[i];
-  } else {
-    double r[8];
-    for (int jj = 0; jj < 8; ++jj) r[jj] = x[jj];
-    int i;
-    for (i = 8; i < m - (m % 8); i += 8)
-      for (int jj = 0; jj < 8; ++jj) r[jj] += x[i + jj];
-    rest = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < m; ++i) rest += x[i];
-  }
-  return rest;
-}
-
-// ---------------------------------------------------------------------------
-// scalar bookkeeping (one thread)
-
-template <int D, bool HERM>
-__device__ void record(const KParams& P, long long step) {
-  volatile Ctl* c = P.ctl;
-  const long long idx = c->n_rec;
-  if (idx >= P.rec_cap) return;  // host sizes the buffer for a whole chunk
-  P.rec_step[idx] = step;
-  double* pops = P.rec_pops + idx * P.d_full;
-  const double* s0 = P.sig;
-  for (int f = 0; f < P.d_full; ++f) pops[f] = 0.0;
-  for (int i = 0; i < D; ++i) {
-    double re, im;
-    load_sig0<D, HERM>(s0, i, i, re, im);
-    pops[P.block_full[i]] = re;
-  }
-  for (int s = 0; s < P.n_sinks; ++s) pops[P.sink_full[s]] = c->sink_pops[s];
-  if (P.record_matrices) {
-    const int df = P.d_full;
-    double* m = P.rec_mats + idx * df * df * 2;
-    for (int f = 0; f < df * df * 2; ++f) m[f] = 0.0;
-    for (int i = 0; i < D; ++i)
-      for (int j = 0; j < D; ++j) {
-        double re, im;
-        load_sig0<D, HERM>(s0, i, j, re, im);
-        const int f = P.block_full[i] * df + P.block_full[j];
-        m[2 * f] = re;
-        m[2 * f + 1] = im;
-      }
-    for (int s = 0; s < P.n_sinks; ++s) {
-      const int f = P.sink_full[s] * df + P.sink_full[s];
-      m[2 * f] = c->sink_pops[s];
-    }
-  }
-  c->n_rec = idx + 1;
-}
-
-// stop policy evaluated before step `step` (heom.py:359-368)
-template <int D, bool HERM>
-__device__ void check_stop(const KParams& P, long long step) {
-  volatile Ctl* c = P.ctl;
-  const double t = (double)step * P.dt;
-  int st = ST_RUNNING;
-  if (P.has_t_end && t >= P.t_end - 1e-9) {
-    st = ST_T_END;
-  } else if (P.has_residual) {
-    double diag[MAXD];
-    for (int k = 0; k < P.n_site_pos; ++k) {
-      double re, im;
-      load_sig0<D, HERM>(P.sig, P.site_pos[k], P.site_pos[k], re, im);
-      diag[k] = re;
-    }
-    if (np_sum(diag, P.n_site_pos) <= P.residual) st = ST_RESIDUAL;
-  }
-  if (st == ST_RUNNING && !P.has_t_end && t >= P.hard_cap) {
-    c->status = ST_HARDCAP;
-    return;
-  }
-  if (st != ST_RUNNING) {
-    if (step % P.stride != 0) record<D, HERM>(P, step);
-    c->status = st;
-  }
-}
-
-template <int D, bool HERM>
-__device__ void finish_step(const KParams& P, long long step) {
-  volatile Ctl* c = P.ctl;
-  c->blocks_done = 0;
-  c->step = step;
-  for (int s = 0; s < P.n_sinks; ++s)
-    c->sink_pops[s] += (P.dt / 6.0) * (c->r[0][s] + 2.0 * (c->r[1][s] + c->r[2][s]) + c->r[3][s]);
-  double m0 = 0.0;
-  for (int i = 0; i < D; ++i)
-    for (int j = 0; j < D; ++j) {
-      double re, im;
-      load_sig0<D, HERM>(P.sig, i, j, re, im);
-      const double a2 = re * re + im * im;
-      if (a2 > m0) m0 = a2;
-    }
-  const bool full = step % 25 == 0;
-  double mall = 0.0;
-  if (full) {
-    mall = __longlong_as_double((long long)c->maxabs2_bits);
-    c->maxabs2_bits = 0ull;
-  }
-  if (m0 > P.blow2 || (full && mall > P.blow2)) {
-    c->status = ST_DIVERGED;
-    return;
-  }
-  if (step % P.stride == 0) record<D, HERM>(P, step);
-  check_stop<D, HERM>(P, step);
-}
 
 // ---------------------------------------------------------------------------
 // the stage kernel
@@ -420,19 +228,17 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
       s_last = prev == gridDim.x - 1;
     }
     __syncthreads();
-    if (s_last && threadIdx.x == 0) {
+    if (s_last && (threadIdx.x >> 5) == 0) {
       __threadfence();
-      ctl->launches = ctl->launches + 4;
-      finish_step<D, HERM>(P, step_next);
+      if (threadIdx.x == 0) ctl->launches = ctl->launches + 4;
+      finish_step_warp<D, HERM>(P, step_next);
     }
   }
 }
 
 template <int D, bool HERM>
 __global__ void k_init(const KParams P) {
-  // t = 0 sample + stop policy before the first step (heom.py:355-368)
-  record<D, HERM>(P, 0);
-  check_stop<D, HERM>(P, 0);
+  init_warp<D, HERM>(P);
 }
 
 // ---------------------------------------------------------------------------
@@ -570,6 +376,7 @@ static cudaError_t dispatch_stage(int stage, const KParams& p, cudaStream_t s) {
   return cudaErrorInvalidValue;
 
 cudaError_t launch_stage(int stage, const KParams& p, cudaStream_t s) {
+  if (p.fast && stage >= 1) return launch_fast(stage, p, s);
   HB_DISPATCH_D(dispatch_stage, stage, p, s)
 }
 
@@ -579,7 +386,7 @@ cudaError_t configure_stages(const KParams& p) { HB_DISPATCH_D(configure_impl, p
 
 template <int D, bool HERM>
 static cudaError_t init_impl(const KParams& p, cudaStream_t s) {
-  k_init<D, HERM><<<1, 1, 0, s>>>(p);
+  k_init<D, HERM><<<1, 32, 0, s>>>(p);
   return cudaGetLastError();
 }
 cudaError_t launch_init(const KParams& p, cudaStream_t s) { HB_DISPATCH_D(init_impl, p, s) }

@@ -112,7 +112,8 @@ class DeviceRun:
     def __init__(self, ops: BlockOperands, n_max: int, dt_fs: float, t_end_fs=None,
                  residual=None, hard_cap_fs: float = 200_000.0, record_stride: int = 1,
                  record_matrices: bool = False, blowup_norm: float = 1e6, device: int = 0,
-                 layout: str = "auto", ordering: str = "lex", chunk_steps: int = 0):
+                 layout: str = "auto", ordering: str = "lex", chunk_steps: int = 0,
+                 kernel: str = "auto"):
         N.require_device(device)
         if ops.d > 8:
             raise ValueError("block dimension above 8 is not supported by the device kernels")
@@ -152,6 +153,7 @@ class DeviceRun:
         p.layout = N.HB_LAYOUT[layout]
         p.ordering = N.HB_ORDER[ordering]
         p.chunk_steps = int(chunk_steps)
+        p.kernel_variant = N.HB_KERNEL[kernel]
         self._params = p
         handle = C.c_void_p()
         N.check(N.lib().hb_create(C.byref(p), C.byref(handle)), "hb_create")

@@ -48,7 +48,9 @@ class PropagationConfig:
       layout       'auto' (Hermitian-packed when rho0 is exactly Hermitian),
                    'hermitian' or 'general';
       ordering     device ADO order: 'lex' (locality) or 'reference';
-      chunk_steps  RK4 steps per CUDA-graph launch (0 = library default).
+      chunk_steps  RK4 steps per CUDA-graph launch (0 = library default);
+      kernel       'auto' (unrolled thread-per-ADO kernel when the shape allows)
+                   or 'generic' (runtime-shaped tile kernel).
     """
 
     dt_fs: float = 2.5
@@ -65,6 +67,7 @@ class PropagationConfig:
     layout: str = "auto"
     ordering: str = "lex"
     chunk_steps: int = 0
+    kernel: str = "auto"
 
     def __post_init__(self):
         if self.dt_fs <= 0:
@@ -85,6 +88,8 @@ class PropagationConfig:
             raise ValueError("layout must be 'auto', 'hermitian' or 'general'")
         if self.ordering not in N.HB_ORDER:
             raise ValueError("ordering must be 'lex' or 'reference'")
+        if self.kernel not in N.HB_KERNEL:
+            raise ValueError("kernel must be 'auto' or 'generic'")
 
     @property
     def dtype(self):
@@ -193,7 +198,8 @@ def propagate_from(system: ExcitonSystem, bath: BathParams, rates: MarkovRates,
                     residual=config.residual, hard_cap_fs=config.hard_cap_fs,
                     record_stride=config.record_stride, record_matrices=config.record_matrices,
                     blowup_norm=config.blowup_norm, device=config.device, layout=config.layout,
-                    ordering=config.ordering, chunk_steps=config.chunk_steps)
+                    ordering=config.ordering, chunk_steps=config.chunk_steps,
+                    kernel=config.kernel)
     with run:
         run.set_rho0(block, [float(rho0[s, s].real) for s in ops.sinks])
         rc = run.run()

@@ -136,14 +136,18 @@ def test_hard_cap_message(golden_traj):
     assert str(exc.value) == meta["hardcap"]["message"]
 
 
-def test_layouts_and_orderings_agree():
-    base = dict(dt_fs=2.5, n_max=3, t_end_fs=300.0, residual=None)
-    ref = xf.propagate(FMO, BATH300, RATES, xf.PropagationConfig(**base), 1).populations
+@pytest.mark.parametrize("K", [0, 1])
+def test_layouts_orderings_kernels_agree(K):
+    base = dict(dt_fs=2.5, n_max=3, t_end_fs=300.0, residual=None, n_matsubara=K,
+                record_matrices=True, record_stride=10)
+    ref = xf.propagate(FMO, BATH300, RATES, xf.PropagationConfig(**base), 1)
     for layout in ("hermitian", "general"):
         for ordering in ("lex", "reference"):
-            cfg = xf.PropagationConfig(**base, layout=layout, ordering=ordering)
-            p = xf.propagate(FMO, BATH300, RATES, cfg, 1).populations
-            assert np.max(np.abs(p - ref)) < 1e-13, (layout, ordering)
+            for kernel in ("auto", "generic"):
+                cfg = xf.PropagationConfig(**base, layout=layout, ordering=ordering, kernel=kernel)
+                t = xf.propagate(FMO, BATH300, RATES, cfg, 1)
+                assert np.max(np.abs(t.populations - ref.populations)) < 1e-13, (layout, ordering)
+                assert np.max(np.abs(t.matrices - ref.matrices)) < 1e-13, (layout, ordering)
 
 
 def test_chunking_does_not_change_results():
