@@ -47,7 +47,7 @@ extern "C" {
 #define HB_KERNEL_AUTO 0       /* unrolled thread-per-ADO kernel when the shape allows */
 #define HB_KERNEL_GENERIC 1    /* runtime-shaped tile kernel (any d, K, layout)        */
 
-#define HB_MAX_D 8
+#define HB_MAX_D 9
 #define HB_MAX_KP1 8
 #define HB_MAX_SINKS 4
 #define HB_MAX_SINK_TERMS 32
@@ -127,6 +127,16 @@ int hb_rhs(double* out, const double* sig, int64_t n_tot, int d, const double* h
            const int32_t* site_of, const int32_t* plus, const int32_t* minus, int modes,
            const double* nvec, const double* tier_damp, double a_comm, double b_anti,
            const double* decay, int device);
+
+/* heom.py:175-204 heom_rhs: the dense semantic definition on the FULL basis
+ * (sinks included): hb_rhs plus the Lindblad refill of the sink populations,
+ * out[dst,dst] += rate * sig[src,src] for every (rate, src, dst) channel
+ * (heom.py:146).  d up to HB_MAX_D (9 = the FMO basis). */
+int hb_heom_rhs(double* out, const double* sig, int64_t n_tot, int d, const double* h,
+                const int32_t* site_of, const int32_t* plus, const int32_t* minus, int modes,
+                const double* nvec, const double* tier_damp, double a_comm, double b_anti,
+                const double* decay, int n_refill, const int32_t* refill_dst,
+                const int32_t* refill_src, const double* refill_rate, int device);
 
 /* _kernels.py:61-65 add_scaled: out = x + c*y over n complex elements. */
 int hb_add_scaled(double* out, const double* x, const double* y, double c, int64_t n,

@@ -25,7 +25,7 @@ HB_KERNEL = {"auto": 0, "generic": 1}
 
 #: every symbol include/heom_b200.h declares (checked by the CPU test-suite)
 EXPORTS = ("hb_last_error", "hb_device_count", "hb_hierarchy_size", "hb_graph_build",
-           "hb_rhs", "hb_add_scaled", "hb_rk4_update", "hb_max_abs2", "hb_create",
+           "hb_rhs", "hb_heom_rhs", "hb_add_scaled", "hb_rk4_update", "hb_max_abs2", "hb_create",
            "hb_destroy", "hb_set_rho0", "hb_run", "hb_get_records", "hb_get_state",
            "hb_get_sigma0", "hb_time_steps", "hb_launch_count")
 
@@ -77,6 +77,8 @@ def lib():
         "hb_hierarchy_size": (_i64, [_i, _i]),
         "hb_graph_build": (_i, [_i, _i, _i, _p, _p, _p, _p, _p]),
         "hb_rhs": (_i, [_p, _p, _i64, _i, _p, _p, _p, _p, _i, _p, _p, _d, _d, _p, _i]),
+        "hb_heom_rhs": (_i, [_p, _p, _i64, _i, _p, _p, _p, _p, _i, _p, _p, _d, _d, _p, _i, _p, _p,
+                             _p, _i]),
         "hb_add_scaled": (_i, [_p, _p, _p, _d, _i64, _i]),
         "hb_rk4_update": (_i, [_p, _p, _p, _p, _p, _d, _i64, _i]),
         "hb_max_abs2": (_i, [_p, _i64, C.POINTER(_d), _i]),

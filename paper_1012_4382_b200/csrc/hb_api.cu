@@ -169,11 +169,13 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
-int hb_rhs(double* out, const double* sig, int64_t n_tot, int d, const double* h,
-           const int32_t* site_of, const int32_t* plus, const int32_t* minus, int modes,
-           const double* nvec, const double* tier_damp, double a_comm, double b_anti,
-           const double* decay, int device) {
-  if (d < 1 || d > MAXD) return fail(HB_ERR_ARG, "block dimension must be 1..8");
+static int rhs_impl(double* out, const double* sig, int64_t n_tot, int d, const double* h,
+                    const int32_t* site_of, const int32_t* plus, const int32_t* minus, int modes,
+                    const double* nvec, const double* tier_damp, double a_comm, double b_anti,
+                    const double* decay, int n_refill, const int32_t* refill_dst,
+                    const int32_t* refill_src, const double* refill_rate, int device) {
+  if (n_refill < 0 || n_refill > MAXT) return fail(HB_ERR_ARG, "too many refill channels");
+  if (d < 1 || d > MAXD) return fail(HB_ERR_ARG, "block dimension must be 1..9");
   if (n_tot < 1 || n_tot > INT32_MAX) return fail(HB_ERR_ARG, "bad n_tot");
   if (modes < 1 || modes > MAX_MODES) return fail(HB_ERR_ARG, "bad mode count");
   std::vector<uint8_t> nv((size_t)n_tot * modes);
@@ -206,6 +208,14 @@ int hb_rhs(double* out, const double* sig, int64_t n_tot, int d, const double* h
   }
   p.a[0] = a_comm;
   p.b[0] = b_anti;
+  p.n_refill = n_refill;
+  for (int q = 0; q < n_refill; ++q) {
+    if (refill_dst[q] < 0 || refill_dst[q] >= d || refill_src[q] < 0 || refill_src[q] >= d)
+      return fail(HB_ERR_ARG, "refill channel out of range");
+    p.refill_dst[q] = refill_dst[q];
+    p.refill_src[q] = refill_src[q];
+    p.refill_rate[q] = refill_rate[q];
+  }
   const size_t n_pad = (size_t)gt.n_tiles * TILE;
   const size_t ref_bytes = (size_t)n_tot * d * d * 2 * sizeof(double);
   const size_t dev_bytes = n_pad * p.n_planes * sizeof(double);
@@ -230,6 +240,23 @@ int hb_rhs(double* out, const double* sig, int64_t n_tot, int d, const double* h
   CK(cudaMemcpyAsync(out, dref.p, ref_bytes, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return HB_OK;
+}
+
+int hb_rhs(double* out, const double* sig, int64_t n_tot, int d, const double* h,
+           const int32_t* site_of, const int32_t* plus, const int32_t* minus, int modes,
+           const double* nvec, const double* tier_damp, double a_comm, double b_anti,
+           const double* decay, int device) {
+  return rhs_impl(out, sig, n_tot, d, h, site_of, plus, minus, modes, nvec, tier_damp, a_comm,
+                  b_anti, decay, 0, nullptr, nullptr, nullptr, device);
+}
+
+int hb_heom_rhs(double* out, const double* sig, int64_t n_tot, int d, const double* h,
+                const int32_t* site_of, const int32_t* plus, const int32_t* minus, int modes,
+                const double* nvec, const double* tier_damp, double a_comm, double b_anti,
+                const double* decay, int n_refill, const int32_t* refill_dst,
+                const int32_t* refill_src, const double* refill_rate, int device) {
+  return rhs_impl(out, sig, n_tot, d, h, site_of, plus, minus, modes, nvec, tier_damp, a_comm,
+                  b_anti, decay, n_refill, refill_dst, refill_src, refill_rate, device);
 }
 
 static int elementwise(int op, double* out, const double* x, const double* y, const double* z,
@@ -324,7 +351,7 @@ int hb_create(const hb_params* P, hb_handle** out) {
   *out = nullptr;
   if (!P) return fail(HB_ERR_ARG, "null params");
   const hb_params& q = *P;
-  if (q.d < 1 || q.d > MAXD) return fail(HB_ERR_ARG, "block dimension must be 1..8");
+  if (q.d < 1 || q.d > MAXD) return fail(HB_ERR_ARG, "block dimension must be 1..9");
   if (q.kp1 < 1 || q.kp1 > MAXKP1) return fail(HB_ERR_ARG, "n_matsubara must be 0..7");
   if (q.n_max > 255) return fail(HB_ERR_ARG, "n_max > 255 is not supported");
   if (q.n_sinks < 0 || q.n_sinks > MAXS) return fail(HB_ERR_ARG, "too many sinks");

@@ -77,6 +77,9 @@ struct KParams {
   int sink_full[MAXS];
   int full2blk[MAXFULL];     // full index -> block position or -1
   int full2sink[MAXFULL];    // full index -> sink slot or -1
+  int n_refill;              // dense path only: out[dst,dst] += rate * sig[src,src]
+  int refill_dst[MAXT], refill_src[MAXT];
+  double refill_rate[MAXT];
   int has_t_end, has_residual, record_matrices, hermitian;
   double t_end, residual, hard_cap, blow2;
   long long stride;

@@ -180,6 +180,14 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
       }
     }
 
+    if (i == j) {  // Lindblad refill of sink levels (dense path, heom.py:146)
+      for (int q = 0; q < P.n_refill; ++q)
+        if (P.refill_dst[q] == i) {
+          const int src = P.refill_src[q];
+          ar += P.refill_rate[q] * s_re[src][src][lane];
+          ai += P.refill_rate[q] * s_im[src][src][lane];
+        }
+    }
     double yr, yi;
     if (STAGE == 0) {
       yr = ar;
@@ -372,6 +380,7 @@ static cudaError_t dispatch_stage(int stage, const KParams& p, cudaStream_t s) {
     case 6: return p.hermitian ? FN<6, true>(__VA_ARGS__) : FN<6, false>(__VA_ARGS__); \
     case 7: return p.hermitian ? FN<7, true>(__VA_ARGS__) : FN<7, false>(__VA_ARGS__); \
     case 8: return p.hermitian ? FN<8, true>(__VA_ARGS__) : FN<8, false>(__VA_ARGS__); \
+    case 9: return p.hermitian ? FN<9, true>(__VA_ARGS__) : FN<9, false>(__VA_ARGS__); \
   }                                                                              \
   return cudaErrorInvalidValue;
 

@@ -115,8 +115,8 @@ class DeviceRun:
                  layout: str = "auto", ordering: str = "lex", chunk_steps: int = 0,
                  kernel: str = "auto"):
         N.require_device(device)
-        if ops.d > 8:
-            raise ValueError("block dimension above 8 is not supported by the device kernels")
+        if ops.d > 9:
+            raise ValueError("block dimension above 9 is not supported by the device kernels")
         self.ops = ops
         self.dt = dt_fs
         self.record_matrices = record_matrices

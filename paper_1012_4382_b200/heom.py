@@ -27,6 +27,7 @@ from .engine import (BlockOperands, DeviceRun, bath_coefficients, bath_modes,  #
 from .hierarchy import HierarchyGraph, hierarchy_size
 from .model import BathParams, ExcitonSystem, MarkovRates
 from .observables import Trajectory, trapping_time
+from .units import ANGFREQ_RAD_FS
 
 
 class PropagationDiverged(RuntimeError):
@@ -135,6 +136,68 @@ def bath_backaction(system: ExcitonSystem, site_label: int, sigma: np.ndarray,
     out[idx, :] += (b + 1j * a) * sigma[idx, :]
     out[:, idx] += (b - 1j * a) * sigma[:, idx]
     return out
+
+
+def heom_rhs(state: HierarchyState, graph: HierarchyGraph, system: ExcitonSystem,
+             bath: BathParams, rates: MarkovRates) -> np.ndarray:
+    """d sigma / dt of the full hierarchy on the FULL basis, sinks included
+    (the dense semantic definition, heom.py:175-204), evaluated on the GPU by the
+    generic stage kernel with the Lindblad sink refill (hb_heom_rhs)."""
+    N.require_device(0)
+    sigma = np.ascontiguousarray(state.sigma, dtype=np.complex128)
+    n_tot, d, _ = sigma.shape
+    h = np.ascontiguousarray(system.h_cm1 * ANGFREQ_RAD_FS)
+    site_of = np.full(d, -1, np.int32)
+    for slot, idx in enumerate(system.site_indices):
+        site_of[idx] = slot
+    decay = np.zeros(d)
+    dst, src, rate = [], [], []
+    for r, b_, a_ in loss_channels(system, rates):
+        decay[b_] += r
+        dst.append(a_)
+        src.append(b_)
+        rate.append(r)
+    a, b = bath_coefficients(bath)
+    plus = np.ascontiguousarray(graph.plus, dtype=np.int32)
+    minus = np.ascontiguousarray(graph.minus, dtype=np.int32)
+    nvec = np.ascontiguousarray(graph.indices, dtype=np.float64)
+    tier_damp = np.ascontiguousarray(graph.tiers * bath.gamma_fs1, dtype=np.float64)
+    dst = np.array(dst or [0], np.int32)
+    src = np.array(src or [0], np.int32)
+    rate = np.array(rate or [0.0])
+    out = np.empty_like(sigma)
+    rc = N.lib().hb_heom_rhs(N.ptr(out), N.ptr(sigma), n_tot, d, N.ptr(h), N.ptr(site_of),
+                             N.ptr(plus), N.ptr(minus), plus.shape[1], N.ptr(nvec),
+                             N.ptr(tier_damp), float(a), float(b), N.ptr(decay),
+                             len(loss_channels(system, rates)),
+                             N.ptr(dst), N.ptr(src), N.ptr(rate), 0)
+    N.check(rc, "hb_heom_rhs")
+    return out
+
+
+def rk4_step(state: HierarchyState, graph: HierarchyGraph, system: ExcitonSystem,
+             bath: BathParams, rates: MarkovRates, dt_fs: float,
+             blowup_norm: float = 1e6) -> HierarchyState:
+    """One classical RK4 step of the dense definition (heom.py:207-219); the
+    stage combinations run on the device through the Level-2 kernel shims."""
+    from . import kernels
+    s = np.ascontiguousarray(state.sigma, dtype=np.complex128)
+    flat = s.reshape(-1)
+    k1 = heom_rhs(state, graph, system, bath, rates)
+    tmp = np.empty_like(s)
+    kernels.add_scaled(tmp.reshape(-1), flat, k1.reshape(-1), 0.5 * dt_fs)
+    k2 = heom_rhs(HierarchyState(tmp.copy()), graph, system, bath, rates)
+    kernels.add_scaled(tmp.reshape(-1), flat, k2.reshape(-1), 0.5 * dt_fs)
+    k3 = heom_rhs(HierarchyState(tmp.copy()), graph, system, bath, rates)
+    kernels.add_scaled(tmp.reshape(-1), flat, k3.reshape(-1), dt_fs)
+    k4 = heom_rhs(HierarchyState(tmp.copy()), graph, system, bath, rates)
+    new = s.copy()
+    kernels.rk4_update(new.reshape(-1), k1.reshape(-1), k2.reshape(-1), k3.reshape(-1),
+                       k4.reshape(-1), dt_fs / 6.0)
+    if kernels.max_abs2(new.reshape(-1)) > blowup_norm * blowup_norm:
+        raise PropagationDiverged(
+            f"matrix norm exceeded {blowup_norm:g} at t = {state.time_fs + dt_fs} fs")
+    return HierarchyState(sigma=new, time_fs=state.time_fs + dt_fs)
 
 
 def _check_rho0(system: ExcitonSystem, rho0) -> np.ndarray:

@@ -121,6 +121,22 @@ def rhs_cases():
     np.savez_compressed(OUT / "rhs_cases.npz", **arrays)
 
 
+def dense_cases():
+    """heom.heom_rhs / rk4_step (heom.py:175-219): the dense 9x9 definition."""
+    fmo = xf.build_fmo_system()
+    bath = xf.BathParams.from_timescale(35.0, 166.0, 300.0)
+    rates = xf.MarkovRates.from_inverse_ps(2.5, 250.0)
+    graph = _graph(7, 2)
+    rng = np.random.default_rng(5)
+    sig = rng.standard_normal((graph.n_tot, 9, 9)) + 1j * rng.standard_normal((graph.n_tot, 9, 9))
+    out = xf.heom_rhs(xf.HierarchyState(sig), graph, fmo, bath, rates)
+    state = xf.HierarchyState.initial(graph, fmo, np.diag([0, 1.0] + [0] * 7).astype(complex))
+    for _ in range(40):
+        state = xf.rk4_step(state, graph, fmo, bath, rates, 2.5)
+    np.savez_compressed(OUT / "dense_cases.npz", sig=sig, out=out, rk40_sigma=state.sigma,
+                        rk40_time=np.float64(state.time_fs))
+
+
 def _traj_arrays(prefix, traj, arrays, meta):
     arrays[f"{prefix}_times"] = traj.times_fs
     arrays[f"{prefix}_pops"] = traj.populations
@@ -242,12 +258,17 @@ def trajectories(long: bool):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--long", action="store_true", help="only the N_max=6 eta run")
+    ap.add_argument("--dense", action="store_true", help="only the dense heom_rhs fixtures")
     args = ap.parse_args()
+    if args.dense:
+        dense_cases()
+        return
     if args.long:
         trajectories(long=True)
         return
     tables()
     rhs_cases()
+    dense_cases()
     trajectories(long=False)
 
 

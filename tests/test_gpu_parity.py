@@ -235,3 +235,27 @@ def test_large_hierarchy_two_steps_vs_oracle():
     orc.set_threads(1)
     assert np.max(np.abs(traj.populations - ref["populations"])) < 1e-12
     assert np.max(np.abs(traj.final_rho - ref["final_rho"])) < 1e-12
+
+
+# ------------------------------------------------- dense definition (A11)
+
+def test_dense_heom_rhs_matches_reference():
+    g = np.load("tests/golden/dense_cases.npz")
+    graph = xf.enumerate_hierarchy(7, 2)
+    out = xf.heom_rhs(xf.HierarchyState(g["sig"]), graph, FMO, BATH300, RATES)
+    ref = g["out"]
+    assert np.max(np.abs(out - ref)) <= 1e-14 * np.max(np.abs(ref))
+
+
+def test_dense_rk4_matches_reference_and_fast_path():
+    """test_heom.py:120-130: 40 dense RK4 steps vs the fast propagator."""
+    g = np.load("tests/golden/dense_cases.npz")
+    graph = xf.enumerate_hierarchy(7, 2)
+    state = xf.HierarchyState.initial(graph, FMO, site_rho(1))
+    for _ in range(40):
+        state = xf.rk4_step(state, graph, FMO, BATH300, RATES, 2.5)
+    assert state.time_fs == float(g["rk40_time"])
+    assert np.max(np.abs(state.sigma - g["rk40_sigma"])) < 1e-12
+    cfg = xf.PropagationConfig(dt_fs=2.5, n_max=2, t_end_fs=100.0, residual=None)
+    traj = xf.propagate(FMO, BATH300, RATES, cfg, 1)
+    assert np.max(np.abs(traj.populations[-1] - np.real(np.diag(state.rho)))) < 1e-13
