@@ -88,6 +88,8 @@ typedef struct {
     int ordering;             /* HB_ORDER_*                                       */
     int chunk_steps;          /* RK4 steps per CUDA-graph launch (0 = default)    */
     int kernel_variant;       /* HB_KERNEL_*                                      */
+    int tile_begin;           /* sharding: first tile (32 ADOs) this handle owns  */
+    int tile_count;           /* sharding: tiles owned (0 = all from tile_begin)  */
 } hb_params;
 
 typedef struct {
@@ -169,6 +171,9 @@ int hb_run(hb_handle* h, hb_result* res);
 int hb_get_records(hb_handle* h, int64_t* steps, double* pops, double* mats_or_null,
                    int64_t cap);
 
+/* Number of records collected so far (what hb_get_records will return). */
+int64_t hb_record_count(hb_handle* h);
+
 /* Current state in the reference order and layout: sig (n_tot,d,d) complex,
  * sink_pops (n_sinks). */
 int hb_get_state(hb_handle* h, double* sig, double* sink_pops);
@@ -185,6 +190,27 @@ int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms_or
 
 /* Device-side launch count of product kernels since hb_create. */
 int64_t hb_launch_count(hb_handle* h);
+
+/* ---- Sharding (new, no reference counterpart) ----
+ * A handle created with tile_begin/tile_count computes only that contiguous
+ * range of tiles (device order); the handle owning tile 0 (the root, ADO 0)
+ * does the sink integration, records and the full stop policy.  Between stages
+ * the caller moves halo tiles of the stage output buffer between shards:
+ * buffer index 0 = sigma, 1 = Y2, 2 = Y3, 3 = Y4 (stage s writes buffer s % 4).
+ * Sharded runs support the t_end stop policy. */
+int hb_run_stage(hb_handle* h, int stage);          /* enqueue one stage kernel (1..4) */
+int hb_sync(hb_handle* h, int* status, int64_t* step);  /* wait, drain records, read status */
+/* copy tiles [first, first+count) of buffer `buf` from src into dst (same or peer
+ * device), ordered after everything enqueued on both handles so far */
+int hb_copy_tiles(hb_handle* dst, hb_handle* src, int buf, int first_tile, int n_tiles);
+/* NCCL halo exchange (libnccl loaded at run time); id = ncclUniqueId (128 bytes) */
+int hb_nccl_unique_id(char* id128);
+int hb_nccl_init(hb_handle* h, const char* id128, int nranks, int rank);
+/* grouped ncclSend/ncclRecv of tile runs of buffer `buf` on the handle's stream:
+ * entry i sends (is_send[i] = 1) or receives tiles [first[i], first[i]+count[i])
+ * to / from rank peer[i] */
+int hb_exchange(hb_handle* h, int buf, int n, const int32_t* peer, const int32_t* first,
+                const int32_t* count, const int32_t* is_send);
 
 #ifdef __cplusplus
 }

@@ -26,8 +26,9 @@ HB_KERNEL = {"auto": 0, "generic": 1}
 #: every symbol include/heom_b200.h declares (checked by the CPU test-suite)
 EXPORTS = ("hb_last_error", "hb_device_count", "hb_hierarchy_size", "hb_graph_build",
            "hb_rhs", "hb_heom_rhs", "hb_add_scaled", "hb_rk4_update", "hb_max_abs2", "hb_create",
-           "hb_destroy", "hb_set_rho0", "hb_run", "hb_get_records", "hb_get_state",
-           "hb_get_sigma0", "hb_time_steps", "hb_launch_count")
+           "hb_destroy", "hb_set_rho0", "hb_run", "hb_get_records", "hb_record_count", "hb_get_state",
+           "hb_get_sigma0", "hb_time_steps", "hb_launch_count", "hb_run_stage", "hb_sync",
+           "hb_copy_tiles", "hb_nccl_unique_id", "hb_nccl_init", "hb_exchange")
 
 
 class HbParams(C.Structure):
@@ -43,6 +44,7 @@ class HbParams(C.Structure):
         ("record_stride", C.c_int64), ("record_matrices", C.c_int),
         ("blowup_norm", C.c_double), ("device", C.c_int), ("layout", C.c_int),
         ("ordering", C.c_int), ("chunk_steps", C.c_int), ("kernel_variant", C.c_int),
+        ("tile_begin", C.c_int), ("tile_count", C.c_int),
     ]
 
 
@@ -87,10 +89,17 @@ def lib():
         "hb_set_rho0": (_i, [_p, _p, _p]),
         "hb_run": (_i, [_p, C.POINTER(HbResult)]),
         "hb_get_records": (_i, [_p, _p, _p, _p, _i64]),
+        "hb_record_count": (_i64, [_p]),
         "hb_get_state": (_i, [_p, _p, _p]),
         "hb_get_sigma0": (_i, [_p, _p, _p]),
         "hb_time_steps": (_i, [_p, _i64, C.POINTER(_d), _p]),
         "hb_launch_count": (_i64, [_p]),
+        "hb_run_stage": (_i, [_p, _i]),
+        "hb_sync": (_i, [_p, C.POINTER(_i), C.POINTER(_i64)]),
+        "hb_copy_tiles": (_i, [_p, _p, _i, _i, _i]),
+        "hb_nccl_unique_id": (_i, [C.c_char_p]),
+        "hb_nccl_init": (_i, [_p, C.c_char_p, _i, _i]),
+        "hb_exchange": (_i, [_p, _i, _i, _p, _p, _p, _p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

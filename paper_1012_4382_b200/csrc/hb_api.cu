@@ -6,6 +6,7 @@
 // graph of `chunk_steps` RK4 steps (4 stage kernels each).  hb_run replays the
 // graph and synchronises once per chunk to drain records and read the status
 // written by the last CTA of each stage-4 kernel (hb_stage.cu).
+#include <dlfcn.h>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -109,6 +110,8 @@ struct hb_handle {
   std::vector<double> pops, mats;
   int64_t launches = 0;
   bool ready = false;  // rho0 set
+  int own_begin = 0, own_count = 0;  // sharding: owned tile range
+  void* nccl_comm = nullptr;
 };
 
 // definitions take C linkage from the extern "C" declarations in heom_b200.h
@@ -332,9 +335,12 @@ static void free_state(hb_handle* h) {
   h->graph_layout = -1;
 }
 
+static void nccl_destroy(void* comm);
+
 void hb_destroy(hb_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  if (h->nccl_comm) nccl_destroy(h->nccl_comm);
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_state(h);
   h->graph_ref.reset();
@@ -405,6 +411,16 @@ int hb_create(const hb_params* P, hb_handle** out) {
   if (e) return bail(e, "build_graph");
   h->gt = h->graph_ref->gt;
   h->n_tiles = h->gt.n_tiles;
+  h->own_begin = q.tile_begin;
+  h->own_count = q.tile_count > 0 ? q.tile_count : h->n_tiles - q.tile_begin;
+  if (q.tile_begin < 0 || h->own_count < 1 || h->own_begin + h->own_count > h->n_tiles) {
+    hb_destroy(h);
+    return fail(HB_ERR_ARG, "tile range outside the hierarchy");
+  }
+  if (h->own_begin != 0 && !q.has_t_end) {
+    hb_destroy(h);
+    return fail(HB_ERR_ARG, "sharded runs need the t_end stop policy");
+  }
   e = cudaMalloc(&h->ctl, sizeof(Ctl));
   if (e) return bail(e, "cudaMalloc(ctl)");
   const size_t zbytes = (size_t)2 * MAXD * MAXD * TILE * sizeof(double);
@@ -426,9 +442,10 @@ int hb_create(const hb_params* P, hb_handle** out) {
   p.kp1 = q.kp1;
   p.modes = modes;
   p.n_tot = h->n_tot;
-  p.n_tiles = h->n_tiles;
+  p.n_tiles = h->own_count;
   p.n_tiles_total = h->n_tiles;
-  p.tile_begin = 0;
+  p.tile_begin = h->own_begin;
+  p.root = h->own_begin == 0;
   for (int i = 0; i < d; ++i) {
     for (int j = 0; j < d; ++j) p.h[i * MAXD + j] = h->h[i * d + j];
     p.decay[i] = h->decay[i];
@@ -679,6 +696,8 @@ int hb_get_records(hb_handle* h, int64_t* steps, double* pops, double* mats_or_n
   return HB_OK;
 }
 
+int64_t hb_record_count(hb_handle* h) { return h ? (int64_t)h->steps.size() : 0; }
+
 int hb_get_state(hb_handle* h, double* sig, double* sink_pops) {
   if (!h || !h->ready) return fail(HB_ERR_ARG, "no state");
   CK(cudaSetDevice(h->device));
@@ -790,3 +809,152 @@ int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
 }
 
 int64_t hb_launch_count(hb_handle* h) { return h ? h->launches : 0; }
+
+// ---------------------------------------------------------------------------
+// sharding
+
+int hb_run_stage(hb_handle* h, int stage) {
+  if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
+  if (stage < 1 || stage > 4) return fail(HB_ERR_ARG, "stage must be 1..4");
+  CK(cudaSetDevice(h->device));
+  CK(launch_stage(stage, stage_params(h, stage), h->stream));
+  h->launches += 1;
+  return HB_OK;
+}
+
+int hb_sync(hb_handle* h, int* status, int64_t* step) {
+  if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
+  CK(cudaSetDevice(h->device));
+  int rc = sync_ctl(h);
+  if (rc) return rc;
+  rc = drain(h);
+  if (rc) return rc;
+  if (status) *status = h->ctl_host->status;
+  if (step) *step = h->ctl_host->step;
+  return HB_OK;
+}
+
+int hb_copy_tiles(hb_handle* dst, hb_handle* src, int buf, int first_tile, int n_tiles) {
+  if (!dst || !src || !dst->ready || !src->ready) return fail(HB_ERR_ARG, "handles not ready");
+  if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
+  if (dst->n_planes != src->n_planes || dst->n_tiles != src->n_tiles)
+    return fail(HB_ERR_ARG, "handles have different layouts");
+  if (first_tile < 0 || n_tiles < 0 || first_tile + n_tiles > dst->n_tiles)
+    return fail(HB_ERR_ARG, "tile range outside the hierarchy");
+  if (n_tiles == 0) return HB_OK;
+  const size_t tb = (size_t)TILE * dst->n_planes * sizeof(double);
+  cudaEvent_t ev;
+  CK(cudaSetDevice(src->device));
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, src->stream));
+  CK(cudaSetDevice(dst->device));
+  CK(cudaStreamWaitEvent(dst->stream, ev, 0));
+  CK(cudaMemcpyPeerAsync(reinterpret_cast<char*>(dst->buf[buf]) + first_tile * tb, dst->device,
+                         reinterpret_cast<const char*>(src->buf[buf]) + first_tile * tb,
+                         src->device, n_tiles * tb, dst->stream));
+  // the source must not overwrite the tiles before the copy has read them
+  cudaEvent_t done;
+  CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  CK(cudaEventRecord(done, dst->stream));
+  CK(cudaSetDevice(src->device));
+  CK(cudaStreamWaitEvent(src->stream, done, 0));
+  cudaEventDestroy(ev);
+  cudaEventDestroy(done);
+  return HB_OK;
+}
+
+// NCCL, resolved at run time so the library loads without it
+namespace {
+struct NcclApi {
+  typedef int (*GetUniqueId)(void*);
+  typedef int (*CommInitRank)(void**, int, const char*, int);  // ncclUniqueId passed by value
+  typedef int (*SendRecv)(const void*, size_t, int, int, void*, cudaStream_t);
+  typedef int (*Group)();
+  typedef int (*CommDestroy)(void*);
+  typedef const char* (*ErrStr)(int);
+  GetUniqueId get_id = nullptr;
+  void* init_rank = nullptr;
+  SendRecv send = nullptr;
+  SendRecv recv = nullptr;
+  Group group_start = nullptr, group_end = nullptr;
+  CommDestroy destroy = nullptr;
+  ErrStr err = nullptr;
+  bool ok = false;
+};
+struct NcclUniqueId { char internal[128]; };
+typedef int (*CommInitRankById)(void**, int, NcclUniqueId, int);
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return a;
+    a.get_id = (NcclApi::GetUniqueId)dlsym(lib, "ncclGetUniqueId");
+    a.init_rank = dlsym(lib, "ncclCommInitRank");
+    a.send = (NcclApi::SendRecv)dlsym(lib, "ncclSend");
+    a.recv = (NcclApi::SendRecv)dlsym(lib, "ncclRecv");
+    a.group_start = (NcclApi::Group)dlsym(lib, "ncclGroupStart");
+    a.group_end = (NcclApi::Group)dlsym(lib, "ncclGroupEnd");
+    a.destroy = (NcclApi::CommDestroy)dlsym(lib, "ncclCommDestroy");
+    a.err = (NcclApi::ErrStr)dlsym(lib, "ncclGetErrorString");
+    a.ok = a.get_id && a.init_rank && a.send && a.recv && a.group_start && a.group_end;
+    return a;
+  }();
+  return api;
+}
+
+int nccl_fail(int r, const char* where) {
+  const char* m = nccl().err ? nccl().err(r) : "nccl error";
+  return fail(HB_ERR_CUDA, std::string(where) + ": " + m);
+}
+}  // namespace
+
+static void nccl_destroy(void* comm) {
+  if (nccl().destroy) nccl().destroy(comm);
+}
+
+int hb_nccl_unique_id(char* id128) {
+  if (!nccl().ok) return fail(HB_ERR_CUDA, "libnccl.so.2 not found");
+  const int r = nccl().get_id(id128);
+  return r ? nccl_fail(r, "ncclGetUniqueId") : HB_OK;
+}
+
+int hb_nccl_init(hb_handle* h, const char* id128, int nranks, int rank) {
+  if (!h) return fail(HB_ERR_ARG, "null handle");
+  if (!nccl().ok) return fail(HB_ERR_CUDA, "libnccl.so.2 not found");
+  CK(cudaSetDevice(h->device));
+  NcclUniqueId id;
+  std::memcpy(id.internal, id128, sizeof id.internal);
+  void* comm = nullptr;
+  const int r = reinterpret_cast<CommInitRankById>(nccl().init_rank)(&comm, nranks, id, rank);
+  if (r) return nccl_fail(r, "ncclCommInitRank");
+  h->nccl_comm = comm;
+  return HB_OK;
+}
+
+int hb_exchange(hb_handle* h, int buf, int n, const int32_t* peer, const int32_t* first,
+                const int32_t* count, const int32_t* is_send) {
+  if (!h || !h->ready || !h->nccl_comm) return fail(HB_ERR_ARG, "handle without NCCL communicator");
+  if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
+  CK(cudaSetDevice(h->device));
+  const size_t tb = (size_t)TILE * h->n_planes * sizeof(double);
+  int r = nccl().group_start();
+  if (r) return nccl_fail(r, "ncclGroupStart");
+  for (int i = 0; i < n; ++i) {
+    if (first[i] < 0 || count[i] < 0 || first[i] + count[i] > h->n_tiles) {
+      nccl().group_end();
+      return fail(HB_ERR_ARG, "tile range outside the hierarchy");
+    }
+    char* p = reinterpret_cast<char*>(h->buf[buf]) + first[i] * tb;
+    const size_t bytes = count[i] * tb;
+    r = is_send[i] ? nccl().send(p, bytes, /*ncclInt8*/ 0, peer[i], h->nccl_comm, h->stream)
+                   : nccl().recv(p, bytes, /*ncclInt8*/ 0, peer[i], h->nccl_comm, h->stream);
+    if (r) {
+      nccl().group_end();
+      return nccl_fail(r, is_send[i] ? "ncclSend" : "ncclRecv");
+    }
+  }
+  r = nccl().group_end();
+  return r ? nccl_fail(r, "ncclGroupEnd") : HB_OK;
+}

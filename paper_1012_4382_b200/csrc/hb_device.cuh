@@ -212,8 +212,30 @@ __device__ void check_stop_warp(const KParams& P, long long step, const Sig0& s0
   if (lane == 0) c->status = st;
 }
 
+// non-root shard: advance the step, own-range guard every 25 steps, t_end only
+__device__ inline void finish_step_shard(const KParams& P, long long step) {
+  if ((threadIdx.x & 31) != 0) return;
+  volatile Ctl* c = P.ctl;
+  c->blocks_done = 0;
+  c->step = step;
+  if (step % 25 == 0) {
+    const double mall = __longlong_as_double((long long)c->maxabs2_bits);
+    c->maxabs2_bits = 0ull;
+    if (mall > P.blow2) {
+      c->status = ST_DIVERGED;
+      return;
+    }
+  }
+  const double t = (double)step * P.dt;
+  if (P.has_t_end && t >= P.t_end - 1e-9) c->status = ST_T_END;
+}
+
 template <int D, bool HERM>
 __device__ void finish_step_warp(const KParams& P, long long step) {
+  if (!P.root) {
+    finish_step_shard(P, step);
+    return;
+  }
   __shared__ Sig0 s0;
   const int lane = threadIdx.x & 31;
   volatile Ctl* c = P.ctl;
@@ -247,6 +269,10 @@ __device__ void finish_step_warp(const KParams& P, long long step) {
 // t = 0 sample + stop policy before the first step (heom.py:355-368); 1 warp
 template <int D, bool HERM>
 __device__ void init_warp(const KParams& P) {
+  if (!P.root) {
+    if ((threadIdx.x & 31) == 0 && P.has_t_end && 0.0 >= P.t_end - 1e-9) P.ctl->status = ST_T_END;
+    return;
+  }
   __shared__ Sig0 s0;
   sig0_warp<D, HERM>(P, s0);
   record_warp<D>(P, 0, s0);

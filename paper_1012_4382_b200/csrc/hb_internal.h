@@ -46,6 +46,7 @@ struct KParams {
   int d, n_sites, kp1, modes;
   int n_tot, n_tiles, tile_begin, n_planes;
   int n_tiles_total;     // tiles per state buffer (a zero tile follows the last one)
+  int root;              // this launch owns tile 0 (ADO 0): sinks, records, stop policy
   // state (AoSoA: [tile][plane][32] doubles)
   const double* Yin;     // stage input: own tile + gathers
   const double* sig;     // sigma (stages 2-4)

@@ -259,3 +259,30 @@ def test_dense_rk4_matches_reference_and_fast_path():
     cfg = xf.PropagationConfig(dt_fs=2.5, n_max=2, t_end_fs=100.0, residual=None)
     traj = xf.propagate(FMO, BATH300, RATES, cfg, 1)
     assert np.max(np.abs(traj.populations[-1] - np.real(np.diag(state.rho)))) < 1e-13
+
+
+# ------------------------------------------------- sharding (8(e)), one GPU
+
+@pytest.mark.parametrize("n_shards,n_max", [(2, 3), (3, 3), (4, 5)])
+def test_sharded_run_is_bit_exact(n_shards, n_max):
+    from paper_1012_4382_b200.shard import ShardedRun
+    ops = BlockOperands(FMO, BATH300, RATES, 1)
+    rho0 = np.zeros((7, 7), complex)
+    rho0[0, 0] = 1.0
+    with DeviceRun(ops, n_max, 1.0, t_end_fs=30.0, layout="hermitian") as ref:
+        ref.set_rho0(rho0, [0.0, 0.0])
+        assert ref.run() == N.HB_OK
+        steps_ref, pops_ref, _ = ref.records()
+        sig_ref, sinks_ref = ref.sigma0()
+    sr = ShardedRun(ops, n_max, 1.0, 30.0, n_shards)
+    try:
+        assert sum(sr.plan.halo_tiles(q) for q in range(n_shards)) > 0
+        sr.set_rho0(rho0, [0.0, 0.0])
+        assert sr.run() == 1  # t_end
+        steps, pops, _ = sr.records()
+        sig, sinks = sr.runs[0].sigma0()
+    finally:
+        sr.close()
+    assert np.array_equal(steps, steps_ref)
+    assert np.array_equal(pops, pops_ref)          # bit-exact: same kernels, complete halos
+    assert np.array_equal(sig, sig_ref) and np.array_equal(sinks, sinks_ref)
