@@ -195,10 +195,58 @@ def config_dict(world):
             "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
 
 
+def run_sharded(args, dist, world, rank, local):
+    """--shard: config 4 split across the ranks (strong scaling), NCCL halo
+    exchange after every stage (paper_1012_4382_b200/shard.py)."""
+    import torch
+    xf, system, bath, rates = workload()
+    from paper_1012_4382_b200.engine import BlockOperands
+    from paper_1012_4382_b200.shard import NcclShardedRun
+    ops = BlockOperands(system, bath, rates, K_MATS)
+    n_tot = xf.hierarchy_size(ops.modes, N_MAX)
+    sr = NcclShardedRun(ops, N_MAX, DT, 1e15, rank, world, local, dist)
+    rho0 = np.zeros((D, D), complex)
+    rho0[0, 0] = 1.0
+    sr.set_rho0(rho0, [0.0, 0.0])
+    for _ in range(max(3, args.warmup)):
+        sr.enqueue_step()
+    sr.sync()
+    launches0 = N_launch(sr.run_)
+    barrier(dist, local)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sr.enqueue_step()
+    status, _ = sr.sync()
+    wall = time.perf_counter() - t0
+    wall = allmax(dist, wall, f"cuda:{local}")
+    halo = sr.plan.halo_tiles(rank)
+    launches = N_launch(sr.run_) - launches0
+    sr.close()
+    if rank == 0:
+        line = {"metric": METRIC, "value": n_tot * args.steps / wall, "unit": UNIT,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {**config_dict(world), "parallelism": f"sharded x{world} (NCCL halo)",
+                           "halo_tiles_rank0": halo},
+                "gpu_launches": int(launches),
+                "status": status}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+def N_launch(run):
+    return run.launch_count()
+
+
 def run_b200(args):
     world, rank, local = dist_env()
     import torch
     dist = init_dist(world, local, "nccl" if torch.cuda.is_available() else "gloo")
+    if args.shard and world > 1:
+        return run_sharded(args, dist, world, rank, local)
     device = local
     xf, system, bath, rates = workload()
     from paper_1012_4382_b200.engine import BlockOperands, DeviceRun
@@ -299,6 +347,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: split ONE hierarchy across the ranks (NCCL halo exchange) "
+                         "instead of independent replicas")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
