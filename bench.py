@@ -293,12 +293,15 @@ def run_b200(args):
     cfg = xf.PropagationConfig(dt_fs=DT, n_max=N_MAX, t_end_fs=e2e_steps * DT, residual=None,
                                n_matsubara=K_MATS, record_stride=1, device=device)
     xf.propagate(system, bath, rates, cfg, 1)         # warm (module load, graph instantiate)
-    barrier(dist, local)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    traj = xf.propagate(system, bath, rates, cfg, 1)
-    torch.cuda.synchronize()
-    e2e_s = allmax(dist, time.perf_counter() - t0, f"cuda:{device}")
+    best = float("inf")
+    for _ in range(3):                                # best of three end-to-end calls
+        barrier(dist, local)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        traj = xf.propagate(system, bath, rates, cfg, 1)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    e2e_s = allmax(dist, best, f"cuda:{device}")
     e2e_value = n_tot * e2e_steps * world / e2e_s
     h2d = (D * D * 16 + 16 * 4 * D + 64 * D + 512) / e2e_steps  # rho0 tile, operands, ctl
     d2h = traj.populations.shape[1] * 8 + 8 + 256                  # one record + status per step

@@ -933,10 +933,10 @@ static cudaError_t tma_configure() {
     switch (tma_nw()) {
       case 4: return tma_configure_nw<D, KP1, 4>();
       case 16: return tma_configure_nw<D, KP1, 16>();
-      default: break;
+      default: return tma_configure_nw<D, KP1, 8>();
     }
   }
-  return tma_configure_nw<D, KP1, 8>();
+  return cudaSuccess;  // only d = 7 instantiates the TMA variant
 }
 
 template <int D, int KP1, int TNW>
@@ -970,14 +970,229 @@ cudaError_t configure_fast(const KParams& p) {
   return cudaErrorInvalidValue;
 }
 
+
+// ---------------------------------------------------------------------------
+// Mode-major variant: per warp one tile (lane = ADO).
+//   A: damping + commutator from the ADO held in registers -> accumulator in
+//      shared memory ([plane][lane], the packed layout of the state);
+//   B: for each site s, all 2(K+1) link crosses of s are gathered at once (13
+//      elements each, independent loads, nothing else live), summed in
+//      registers and added to the accumulator with one read-modify-write per
+//      cross element -- the gathers of a site are all in flight together
+//      instead of one element at a time;
+//   C: RK epilogue from the accumulator (epilogue tiles were bulk-prefetched
+//      into L2 at kernel start).
+// Per-element term order equals the reference's (row site before column site,
+// raise before lower for each k); only the grouping of the additions differs.
+template <int D, int KP1, int STAGE, int MM_WPC, int MINB>
+__global__ void __launch_bounds__(MM_WPC * 32, MINB) k_mm(const KParams P) {
+  constexpr int NP = D * D;
+  constexpr int M = D * KP1;
+  constexpr int TB = NP * TILE;
+  __shared__ double sAcc[MM_WPC][NP][TILE];
+  __shared__ int sU[MM_WPC][M][TILE];
+  __shared__ int sD[MM_WPC][M][TILE];
+  __shared__ unsigned char sN[MM_WPC][M][TILE];
+  __shared__ double s_red[MM_WPC];
+  __shared__ int s_last;
+
+  volatile Ctl* ctl = P.ctl;
+  if (ctl->status != ST_RUNNING) return;
+  const long long step_next = ctl->step + 1;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int local_tile = blockIdx.x * MM_WPC + w;
+  const bool active = local_tile < P.n_tiles;
+  const int tile = P.tile_begin + local_tile;
+  double maxa2 = 0.0;
+
+  if (active) {
+    const size_t toff = (size_t)tile * TB;
+    if (lane == 0 && P.prefetch) prefetch_epilogue<STAGE>(P, toff, TB * sizeof(double));
+    const size_t tb = toff + lane;
+    double (*acc)[TILE] = sAcc[w];
+    // ---- links, n, damping
+    const int zero_off = P.n_tiles_total * TB;
+    const size_t gb = (size_t)tile * M * TILE + lane;
+    int tk[KP1];
+#pragma unroll
+    for (int k = 0; k < KP1; ++k) tk[k] = 0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int up = __ldg(P.plus + gb + m * TILE);
+      const int dn = __ldg(P.minus + gb + m * TILE);
+      const int n = __ldg(P.nvec + gb + m * TILE);
+      tk[m % KP1] += n;
+      sU[w][m][lane] = up >= 0 && !P.debug ? (up >> 5) * TB + (up & 31) : zero_off;
+      sD[w][m][lane] = dn >= 0 && !P.debug ? (dn >> 5) * TB + (dn & 31) : zero_off;
+      sN[w][m][lane] = (unsigned char)n;
+    }
+    double damp = 0.0;  // heom.py:275, generalised: sum_k nu_k * sum_j n_jk
+#pragma unroll
+    for (int k = 0; k < KP1; ++k) damp += (double)tk[k] * P.nu[k];
+
+    {  // ---- phase A: damping + commutator, ADO in registers
+      double s[NP];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) s[p] = __ldg(P.Yin + tb + p * TILE);
+      if (tile == 0 && lane == 0) {  // sink rates of this stage input (heom.py:282-283)
+        int q = 0;
+        for (int sk = 0; sk < P.n_sinks; ++sk) {
+          double a = 0.0;
+          for (int cc = 0; cc < P.sink_nterms[sk]; ++cc, ++q) {
+            const double v = P.sink_rate[q] * __ldg(P.Yin + P.sink_pos[q] * TILE);
+            a = cc == 0 ? v : a + v;
+          }
+          ctl->r[STAGE - 1][sk] = a;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double cm_im = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l)
+          if (l != i) cm_im += P.h[i * MAXD + l] * sim<D>(s, i, l);
+        acc[i][lane] = -(damp + P.decay[i]) * s[i] - 2.0 * cm_im;
+#pragma unroll
+        for (int j = i + 1; j < D; ++j) {
+          const int pr = Pk<D>::re(i, j), pim = Pk<D>::im(i, j);
+          const double f = -(damp + 0.5 * (P.decay[i] + P.decay[j]));
+          double cr = 0.0, ci = 0.0;
+#pragma unroll
+          for (int l = 0; l < D; ++l) {
+            const double hil = P.h[i * MAXD + l], hlj = P.h[l * MAXD + j];
+            cr += hil * sre<D>(s, l, j) - sre<D>(s, i, l) * hlj;
+            ci += hil * sim<D>(s, l, j) - sim<D>(s, i, l) * hlj;
+          }
+          acc[pr][lane] = f * s[pr] + ci;  // acc += -1j * cm
+          acc[pim][lane] = f * s[pim] - cr;
+        }
+      }
+    }
+    __syncwarp();
+    // ---- phase B: neighbour crosses, one site at a time
+#pragma unroll
+    for (int st = 0; st < D; ++st) {
+      double cre[D], cim[D];
+#pragma unroll
+      for (int o = 0; o < D; ++o) cre[o] = cim[o] = 0.0;
+#pragma unroll
+      for (int k = 0; k < KP1; ++k) {
+        const int m = st * KP1 + k;
+        const double* up = P.Yin + sU[w][m][lane];
+        const double* dn = P.Yin + sD[w][m][lane];
+        const double n = (double)sN[w][m][lane];
+        const double cb = n * P.b[k], ca = n * P.a[k];
+        cre[st] += 2.0 * cb * __ldg(dn + st * TILE);  // diagonal: lower terms twice
+#pragma unroll
+        for (int o = 0; o < D; ++o) {
+          if (o == st) continue;
+          const int a = st < o ? st : o, b = st < o ? o : st;
+          const int pr = Pk<D>::re(a, b), pim = Pk<D>::im(a, b);
+          const double ur = __ldg(up + pr * TILE), ui = __ldg(up + pim * TILE);
+          const double dr = __ldg(dn + pr * TILE), di = __ldg(dn + pim * TILE);
+          if (o > st) {  // element (st, o): st is its row site
+            cre[o] += cb * dr - ca * di - ui;
+            cim[o] += cb * di + ca * dr + ur;
+          } else {       // element (o, st): st is its column site
+            cre[o] += cb * dr + ca * di + ui;
+            cim[o] += cb * di - ca * dr - ur;
+          }
+        }
+      }
+      acc[st][lane] += cre[st];
+#pragma unroll
+      for (int o = 0; o < D; ++o) {
+        if (o == st) continue;
+        const int a = st < o ? st : o, b = st < o ? o : st;
+        acc[Pk<D>::re(a, b)][lane] += cre[o];
+        acc[Pk<D>::im(a, b)][lane] += cim[o];
+      }
+    }
+    __syncwarp();
+    // ---- phase C: RK epilogue
+    const double* own = P.Yin + tb;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      epilogue<STAGE>(P, tb, i, -1, STAGE == 1 || STAGE == 4 ? __ldg(own + i * TILE) : 0.0, 0.0,
+                      acc[i][lane], 0.0, maxa2);
+#pragma unroll
+      for (int j = i + 1; j < D; ++j) {
+        const int pr = Pk<D>::re(i, j), pim = Pk<D>::im(i, j);
+        const double sr = STAGE == 1 || STAGE == 4 ? __ldg(own + pr * TILE) : 0.0;
+        const double si = STAGE == 1 || STAGE == 4 ? __ldg(own + pim * TILE) : 0.0;
+        epilogue<STAGE>(P, tb, pr, pim, sr, si, acc[pr][lane], acc[pim][lane], maxa2);
+      }
+    }
+  }
+
+  if (STAGE == 4) {
+    if (step_next % 25 == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxa2 = fmax(maxa2, __shfl_xor_sync(0xffffffffu, maxa2, o));
+      if (lane == 0) s_red[w] = maxa2;
+      __syncthreads();
+      if (t == 0) {
+        double m = s_red[0];
+        for (int q = 1; q < MM_WPC; ++q) m = fmax(m, s_red[q]);
+        atomicMax(const_cast<unsigned long long*>(&ctl->maxabs2_bits),
+                  (unsigned long long)__double_as_longlong(m));
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) {
+      const unsigned prev = atomicAdd(const_cast<unsigned*>(&ctl->blocks_done), 1u);
+      s_last = prev == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && w == 0) {
+      __threadfence();
+      if (t == 0) ctl->launches = ctl->launches + 4;
+      finish_step_warp<D, true>(P, step_next);
+    }
+  }
+}
+
+template <int D, int KP1, int WPC, int MINB>
+static cudaError_t mm_launch_w(int stage, const KParams& p, cudaStream_t s) {
+  const int grid = (p.n_tiles + WPC - 1) / WPC;
+  switch (stage) {
+    case 1: k_mm<D, KP1, 1, WPC, MINB><<<grid, WPC * 32, 0, s>>>(p); break;
+    case 2: k_mm<D, KP1, 2, WPC, MINB><<<grid, WPC * 32, 0, s>>>(p); break;
+    case 3: k_mm<D, KP1, 3, WPC, MINB><<<grid, WPC * 32, 0, s>>>(p); break;
+    case 4: k_mm<D, KP1, 4, WPC, MINB><<<grid, WPC * 32, 0, s>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// HB_MM_CFG (experiments): 1 = 1 warp/CTA (default, fastest measured), 0 = 2 warps,
+// 3 = 2 warps capped at 128 registers
+static int mm_cfg() {
+  static int v = [] {
+    const char* e = getenv("HB_MM_CFG");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+template <int D, int KP1>
+static cudaError_t mm_launch(int stage, const KParams& p, cudaStream_t s) {
+  switch (mm_cfg()) {
+    case 1: return mm_launch_w<D, KP1, 1, 1>(stage, p, s);
+    case 3: return mm_launch_w<D, KP1, 2, 8>(stage, p, s);
+    default: return mm_launch_w<D, KP1, 2, 1>(stage, p, s);
+  }
+}
+
 bool fast_supported(int d, int kp1) { return d >= 1 && d <= 8 && kp1 >= 1 && kp1 <= 2; }
 
-// HB_FAST_VARIANT (experiments): 1 = sigma in registers (default), 3 = TMA, 2 = warp-split,
-// 0 = column-streamed
+// HB_FAST_VARIANT (experiments): 4 = mode-major (default), 1 = sigma in registers,
+// 3 = TMA, 2 = warp-split, 0 = column-streamed
 static int fast_variant() {
   static int v = [] {
     const char* e = getenv("HB_FAST_VARIANT");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 4;
   }();
   return v;
 }
@@ -1017,6 +1232,7 @@ template <int D, int KP1>
 static cudaError_t fast_dispatch(int stage, const KParams& p, cudaStream_t s) {
   if constexpr (D == 7) {
     const int v = fast_variant();
+    if (v == 4) return mm_launch<D, KP1>(stage, p, s);
     if (v != 3) {
       return fast_minb() == 4 ? legacy_dispatch<D, KP1, 4>(v, stage, p, s)
                               : legacy_dispatch<D, KP1, 1>(v, stage, p, s);
@@ -1026,9 +1242,8 @@ static cudaError_t fast_dispatch(int stage, const KParams& p, cudaStream_t s) {
       case 16: return tma_launch<D, KP1, 16>(stage, p, s);
       default: return tma_launch<D, KP1, 8>(stage, p, s);
     }
-  } else {
-    if (fast_variant() == 1) return legacy_dispatch<D, KP1, 1>(1, stage, p, s);
-    return tma_launch<D, KP1, 8>(stage, p, s);
+  } else {  // other d: the production (mode-major) kernel only
+    return mm_launch_w<D, KP1, 1, 1>(stage, p, s);
   }
 }
 
