@@ -38,8 +38,8 @@ UNIT = "ADO-steps/s"
 N_MAX, K_MATS, DT = 8, 1, 1.0
 D = 7
 S_PACKED = 8 * D * D                      # bytes per Hermitian-packed ADO (392 B)
-B_ALG_STEP = 13 * S_PACKED                # algorithmic state bytes per ADO-step
-B_ALG_STAGE = {1: 2 * S_PACKED, 2: 3 * S_PACKED, 3: 3 * S_PACKED, 4: 5 * S_PACKED}
+B_ALG_STEP = 12 * S_PACKED                # algorithmic state bytes per ADO-step
+B_ALG_STAGE = {1: 2 * S_PACKED, 2: 4 * S_PACKED, 3: 3 * S_PACKED, 4: 3 * S_PACKED}
 SURVEY_B_ALG = 16 * 16 * D * D            # SURVEY 8(d) unpacked-scheme figure, 12,544 B
 
 
@@ -323,7 +323,7 @@ def run_b200(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_unit": "DRAM bytes per RK4 step (4 stage launches), ncu",
                          "alg_bytes_per_step": B_ALG_STEP * n_tot,
-                         "kernel": "k_fast<7,2,stage> (4 launches per RK4 step; achieved = alg bytes / sum of stage times)",
+                         "kernel": "k_mm2<7,2,stage> (4 launches per RK4 step; achieved = alg bytes / sum of stage times)",
                          "bytes_per_ado_step": B_ALG_STEP,
                          "stage_us": [round(1e3 * x, 2) for x in stage_ms],
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},

@@ -95,7 +95,7 @@ struct hb_handle {
   GraphTables gt;                          // copy of graph_ref->gt (non-owning)
   int layout = 0;  // HB_LAYOUT_HERMITIAN / GENERAL once allocated
   int n_planes = 0;
-  double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // sigma, Y2, Y3, Y4
+  double* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // sigma, Y2, Y3, Y4, B
   double* zero_tile = nullptr;  // never written: target of absent links
   Ctl* ctl = nullptr;
   Ctl* ctl_host = nullptr;  // pinned
@@ -512,6 +512,7 @@ static KParams stage_params(hb_handle* h, int stage) {
   p.sig = S;
   p.Y2 = Y2;
   p.Y3 = Y3;
+  p.Bbuf = h->buf[4];
   const double dt = h->prm.dt;
   switch (stage) {
     case 1: p.Yin = S;  p.Yout = Y2; p.coef = 0.5 * dt; break;

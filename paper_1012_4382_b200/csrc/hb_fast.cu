@@ -1185,14 +1185,245 @@ static cudaError_t mm_launch(int stage, const KParams& p, cudaStream_t s) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Production kernel (variant 5): mode-major + the RK base tile delivered by TMA.
+// The stage epilogue needs one base tile per ADO besides its own input; it is
+// bulk-copied (cp.async.bulk, one mbarrier) straight into the shared-memory
+// accumulator at kernel start, so phase A starts from acc = base and every
+// contribution is added pre-scaled by the stage coefficient:
+//   stage 1: Y2 = s + h/2 k1          base = s (own input, from registers)
+//   stage 2: Y3 = s + h/2 k2          base = s;  also B = (Y2 - s)/3 + 2/3 Y3
+//   stage 3: Y4 = s + h k3            base = s
+//   stage 4: s  = B + Y4/3 + h/6 k4   base = B
+// B + Y4/3 = (Y2 + 2Y3 - s + Y4)/3, so s_new = s + h/6 (k1 + 2k2 + 2k3 + k4)
+// (heom.py:381).  B is formed where Y2 is the thread's own input, so the
+// scheme moves 12 state passes per step (2 + 4 + 3 + 3) and no epilogue waits
+// on a load.
+template <int D, int KP1, int STAGE, int MINB>
+__global__ void __launch_bounds__(32, MINB) k_mm2(const KParams P) {
+  constexpr int NP = D * D;
+  constexpr int M = D * KP1;
+  constexpr int TB = NP * TILE;
+  constexpr bool kE1 = STAGE == 2;  // stage 2 parks (Y2 - s)/3 for B
+  __shared__ __align__(128) double sAcc[NP][TILE];
+  __shared__ __align__(128) double sE1[kE1 ? NP : 1][TILE];
+  __shared__ int sU[M][TILE];
+  __shared__ int sD[M][TILE];
+  __shared__ unsigned char sN[M][TILE];
+  __shared__ __align__(8) uint64_t bar;
+
+  volatile Ctl* ctl = P.ctl;
+  if (ctl->status != ST_RUNNING) return;
+  const long long step_next = ctl->step + 1;
+  const int lane = threadIdx.x;
+  const int tile = P.tile_begin + blockIdx.x;
+  const size_t toff = (size_t)tile * TB;
+  const size_t tb = toff + lane;
+  double maxa2 = 0.0;
+  // RK coefficient of this stage's right-hand side
+  const double c = STAGE == 4 ? P.dt / 6.0 : P.coef;
+
+  if (STAGE >= 2 && lane == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, TB * 8u);
+    bulk_g2s(&sAcc[0][0], (STAGE == 4 ? P.Bbuf : P.sig) + toff, TB * 8, &bar);
+  }
+  __syncwarp();  // barrier initialised before any lane waits on it
+  // ---- links, n, damping
+  const int zero_off = P.n_tiles_total * TB;
+  const size_t gb = (size_t)tile * M * TILE + lane;
+  int tk[KP1];
+#pragma unroll
+  for (int k = 0; k < KP1; ++k) tk[k] = 0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int up = __ldg(P.plus + gb + m * TILE);
+    const int dn = __ldg(P.minus + gb + m * TILE);
+    const int n = __ldg(P.nvec + gb + m * TILE);
+    tk[m % KP1] += n;
+    sU[m][lane] = up >= 0 && !P.debug ? (up >> 5) * TB + (up & 31) : zero_off;
+    sD[m][lane] = dn >= 0 && !P.debug ? (dn >> 5) * TB + (dn & 31) : zero_off;
+    sN[m][lane] = (unsigned char)n;
+  }
+  double damp = 0.0;  // heom.py:275, generalised: sum_k nu_k * sum_j n_jk
+#pragma unroll
+  for (int k = 0; k < KP1; ++k) damp += (double)tk[k] * P.nu[k];
+
+  {  // ---- phase A: damping + commutator from the ADO in registers
+    double s[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) s[p] = __ldg(P.Yin + tb + p * TILE);
+    if (tile == 0 && lane == 0) {  // sink rates of this stage input (heom.py:282-283)
+      int q = 0;
+      for (int sk = 0; sk < P.n_sinks; ++sk) {
+        double a = 0.0;
+        for (int cc = 0; cc < P.sink_nterms[sk]; ++cc, ++q) {
+          const double v = P.sink_rate[q] * __ldg(P.Yin + P.sink_pos[q] * TILE);
+          a = cc == 0 ? v : a + v;
+        }
+        ctl->r[STAGE - 1][sk] = a;
+      }
+    }
+    if (STAGE >= 2) mbar_wait(&bar, 0);
+    // base of plane p: own input (stage 1), sigma (2, 3), B + Y4/3 (4)
+    auto base = [&](int p) -> double {
+      if (STAGE == 1) return s[p];
+      if (STAGE == 4) return sAcc[p][lane] + s[p] * (1.0 / 3.0);
+      return sAcc[p][lane];
+    };
+    auto emit_b = [&](int p) {  // stage 2: park (Y2 - s)/3 (own input minus base)
+      if (STAGE == 2) sE1[p][lane] = (s[p] - sAcc[p][lane]) * (1.0 / 3.0);
+    };
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double cm_im = 0.0;
+#pragma unroll
+      for (int l = 0; l < D; ++l)
+        if (l != i) cm_im += P.h[i * MAXD + l] * sim<D>(s, i, l);
+      emit_b(i);
+      sAcc[i][lane] = base(i) + c * (-(damp + P.decay[i]) * s[i] - 2.0 * cm_im);
+#pragma unroll
+      for (int j = i + 1; j < D; ++j) {
+        const int pr = Pk<D>::re(i, j), pim = Pk<D>::im(i, j);
+        const double f = -(damp + 0.5 * (P.decay[i] + P.decay[j]));
+        double cr = 0.0, ci = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+          const double hil = P.h[i * MAXD + l], hlj = P.h[l * MAXD + j];
+          cr += hil * sre<D>(s, l, j) - sre<D>(s, i, l) * hlj;
+          ci += hil * sim<D>(s, l, j) - sim<D>(s, i, l) * hlj;
+        }
+        emit_b(pr);
+        emit_b(pim);
+        sAcc[pr][lane] = base(pr) + c * (f * s[pr] + ci);  // -1j * cm
+        sAcc[pim][lane] = base(pim) + c * (f * s[pim] - cr);
+      }
+    }
+  }
+  __syncwarp();
+  // ---- phase B: neighbour crosses, one site at a time, added pre-scaled by c
+#pragma unroll
+  for (int st = 0; st < D; ++st) {
+    double cre[D], cim[D];
+#pragma unroll
+    for (int o = 0; o < D; ++o) cre[o] = cim[o] = 0.0;
+#pragma unroll
+    for (int k = 0; k < KP1; ++k) {
+      const int m = st * KP1 + k;
+      const double* up = P.Yin + sU[m][lane];
+      const double* dn = P.Yin + sD[m][lane];
+      const double n = (double)sN[m][lane];
+      const double cb = n * P.b[k], ca = n * P.a[k];
+      cre[st] += 2.0 * cb * __ldg(dn + st * TILE);
+#pragma unroll
+      for (int o = 0; o < D; ++o) {
+        if (o == st) continue;
+        const int a = st < o ? st : o, b = st < o ? o : st;
+        const int pr = Pk<D>::re(a, b), pim = Pk<D>::im(a, b);
+        const double ur = __ldg(up + pr * TILE), ui = __ldg(up + pim * TILE);
+        const double dr = __ldg(dn + pr * TILE), di = __ldg(dn + pim * TILE);
+        if (o > st) {
+          cre[o] += cb * dr - ca * di - ui;
+          cim[o] += cb * di + ca * dr + ur;
+        } else {
+          cre[o] += cb * dr + ca * di + ui;
+          cim[o] += cb * di - ca * dr - ur;
+        }
+      }
+    }
+    sAcc[st][lane] += c * cre[st];
+#pragma unroll
+    for (int o = 0; o < D; ++o) {
+      if (o == st) continue;
+      const int a = st < o ? st : o, b = st < o ? o : st;
+      sAcc[Pk<D>::re(a, b)][lane] += c * cre[o];
+      sAcc[Pk<D>::im(a, b)][lane] += c * cim[o];
+    }
+  }
+  __syncwarp();
+  // ---- phase C: store (stage 2 also B = (Y2 - s)/3 + 2/3 Y3)
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const double y = sAcc[p][lane];
+    P.Yout[tb + p * TILE] = y;
+    if (STAGE == 2) P.Bbuf[tb + p * TILE] = sE1[p][lane] + (2.0 / 3.0) * y;
+    if (STAGE == 4) maxa2 = fmax(maxa2, y * y);
+  }
+  if (STAGE == 4) {
+    // |y|^2 per element: diagonal planes are real; an off-diagonal pair adds up
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = i + 1; j < D; ++j) {
+        const double yr = sAcc[Pk<D>::re(i, j)][lane], yi = sAcc[Pk<D>::im(i, j)][lane];
+        maxa2 = fmax(maxa2, yr * yr + yi * yi);
+      }
+    __shared__ int s_last;
+    if (step_next % 25 == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxa2 = fmax(maxa2, __shfl_xor_sync(0xffffffffu, maxa2, o));
+      if (lane == 0)
+        atomicMax(const_cast<unsigned long long*>(&ctl->maxabs2_bits),
+                  (unsigned long long)__double_as_longlong(maxa2));
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      const unsigned prev = atomicAdd(const_cast<unsigned*>(&ctl->blocks_done), 1u);
+      s_last = prev == gridDim.x - 1;
+    }
+    __syncwarp();
+    if (s_last) {
+      __threadfence();
+      if (lane == 0) ctl->launches = ctl->launches + 4;
+      finish_step_warp<D, true>(P, step_next);
+    }
+  }
+}
+
+template <int D, int KP1, int MINB>
+static cudaError_t mm2_launch_b(int stage, const KParams& p, cudaStream_t s) {
+  switch (stage) {
+    case 1: k_mm2<D, KP1, 1, MINB><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 2: k_mm2<D, KP1, 2, MINB><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 3: k_mm2<D, KP1, 3, MINB><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 4: k_mm2<D, KP1, 4, MINB><<<p.n_tiles, 32, 0, s>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// HB_MM2_MINB (experiments): register cap via min resident warps per SM
+static int mm2_minb() {
+  static int v = [] {
+    const char* e = getenv("HB_MM2_MINB");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+template <int D, int KP1>
+static cudaError_t mm2_launch(int stage, const KParams& p, cudaStream_t s) {
+  if constexpr (D == 7) {
+    switch (mm2_minb()) {
+      case 10: return mm2_launch_b<D, KP1, 10>(stage, p, s);
+      case 12: return mm2_launch_b<D, KP1, 12>(stage, p, s);
+      case 16: return mm2_launch_b<D, KP1, 16>(stage, p, s);
+      default: break;
+    }
+  }
+  return mm2_launch_b<D, KP1, 1>(stage, p, s);
+}
+
 bool fast_supported(int d, int kp1) { return d >= 1 && d <= 8 && kp1 >= 1 && kp1 <= 2; }
 
-// HB_FAST_VARIANT (experiments): 4 = mode-major (default), 1 = sigma in registers,
-// 3 = TMA, 2 = warp-split, 0 = column-streamed
+// HB_FAST_VARIANT (experiments): 5 = mode-major + TMA base tile, 12-pass RK (default),
+// 4 = mode-major, 1 = sigma in registers, 3 = TMA, 2 = warp-split, 0 = column-streamed
 static int fast_variant() {
   static int v = [] {
     const char* e = getenv("HB_FAST_VARIANT");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 5;
   }();
   return v;
 }
@@ -1232,6 +1463,7 @@ template <int D, int KP1>
 static cudaError_t fast_dispatch(int stage, const KParams& p, cudaStream_t s) {
   if constexpr (D == 7) {
     const int v = fast_variant();
+    if (v == 5) return mm2_launch<D, KP1>(stage, p, s);
     if (v == 4) return mm_launch<D, KP1>(stage, p, s);
     if (v != 3) {
       return fast_minb() == 4 ? legacy_dispatch<D, KP1, 4>(v, stage, p, s)
@@ -1242,8 +1474,8 @@ static cudaError_t fast_dispatch(int stage, const KParams& p, cudaStream_t s) {
       case 16: return tma_launch<D, KP1, 16>(stage, p, s);
       default: return tma_launch<D, KP1, 8>(stage, p, s);
     }
-  } else {  // other d: the production (mode-major) kernel only
-    return mm_launch_w<D, KP1, 1, 1>(stage, p, s);
+  } else {  // other d: the production kernel only
+    return mm2_launch<D, KP1>(stage, p, s);
   }
 }
 

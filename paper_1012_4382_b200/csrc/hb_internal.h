@@ -53,6 +53,7 @@ struct KParams {
   const double* Y2;      // stage 4
   const double* Y3;      // stage 4
   double* Yout;          // Y_{s+1} (stages 1-3), sigma (stage 4), k (rhs-only)
+  double* Bbuf;          // B-scheme kernels: B = (Y2 - s)/3 + 2/3 Y3 (written at stage 2)
   // tables (AoSoA: [tile][mode][32])
   const int32_t* plus;
   const int32_t* minus;
