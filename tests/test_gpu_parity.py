@@ -286,3 +286,55 @@ def test_sharded_run_is_bit_exact(n_shards, n_max):
     assert np.array_equal(steps, steps_ref)
     assert np.array_equal(pops, pops_ref)          # bit-exact: same kernels, complete halos
     assert np.array_equal(sig, sig_ref) and np.array_equal(sinks, sinks_ref)
+
+
+# ------------------------------------------------- sweeps (8(f) rank 2)
+
+def test_sweep_is_worker_count_invariant():
+    """cli.py:279-284 / test_cli.py:182-190: results independent of the worker count."""
+    from paper_1012_4382_b200.sweep import SweepPoint, fmo_point_runner, run_points
+    cfg = xf.PropagationConfig(dt_fs=5.0, n_max=2, residual=1e-5, record_stride=20)
+    pts = [SweepPoint(temperature_k=t, lam_cm1=lam) for t in (77.0, 300.0) for lam in (20.0, 55.0)]
+    runner = fmo_point_runner(cfg, RATES)
+    seq = run_points(pts, runner, workers=1)
+    par = run_points(pts, runner, workers=4)
+    assert [r.point for r in par] == pts
+    for a, b in zip(seq, par):
+        assert a.efficiency == b.efficiency and a.trapping_time_ps == b.trapping_time_ps
+        assert a.steps == b.steps and a.stop_reason == "residual"
+    ref = orc.propagate_from(FMO, xf.BathParams.from_timescale(55.0, 166.0, 300.0), RATES, cfg,
+                             site_rho(1))
+    assert abs(seq[3].efficiency - ref["populations"][-1, 8]) < 1e-10
+
+
+# ------------------------------------------------- other shapes vs the oracle
+
+def _random_system(n, seed, ground=False):
+    rng = np.random.default_rng(seed)
+    a = rng.normal(0.0, 60.0, (n, n))
+    h = (a + a.T) / 2.0
+    h[np.diag_indices(n)] = rng.normal(0.0, 120.0, n)
+    if ground:
+        full = np.zeros((n + 1, n + 1))
+        full[1:, 1:] = h
+        return xf.ExcitonSystem(h_cm1=full, site_indices=tuple(range(1, n + 1)), ground_index=0)
+    return xf.ExcitonSystem(h_cm1=h, site_indices=tuple(range(n)))
+
+
+@pytest.mark.parametrize("n,K,n_max,ground", [(1, 0, 5, False), (3, 1, 3, True), (5, 1, 3, False),
+                                              (8, 0, 2, False), (9, 0, 1, False), (4, 2, 2, False)])
+def test_other_shapes_match_oracle(n, K, n_max, ground):
+    system = _random_system(n, 100 + n, ground)
+    rates = xf.MarkovRates(0.0, 1.0 / 50000.0) if ground else xf.MarkovRates.none()
+    bath = xf.BathParams.from_timescale(25.0, 120.0, 250.0)
+    cfg = xf.PropagationConfig(dt_fs=1.0, n_max=n_max, t_end_fs=60.0, residual=None,
+                               n_matsubara=K, record_stride=7, record_matrices=True)
+    d = system.dimension
+    rho0 = np.zeros((d, d), complex)
+    first = system.site_indices[0]
+    rho0[first, first] = 1.0
+    traj = xf.propagate_from(system, bath, rates, cfg, rho0)
+    ref = orc.propagate_from(system, bath, rates, cfg, rho0)
+    assert np.array_equal(traj.times_fs, ref["times_fs"])
+    assert np.max(np.abs(traj.populations - ref["populations"])) < 1e-10
+    assert np.max(np.abs(traj.matrices - ref["matrices"])) < 1e-10

@@ -120,3 +120,39 @@ def test_gloo_halo_exchange_reproduces_unsharded_rhs():
     assert [r[1] for r in res] == [True, True]
     assert sum(r[2] for r in res) == orc.hierarchy_size(14, 3)
     assert all(r[3] > 0 for r in res)
+
+
+def test_sweep_point_dealing():
+    from paper_1012_4382_b200.sweep import shard_points, temperature_lambda_grid
+    pts = temperature_lambda_grid()
+    assert len(pts) == 64
+    dealt = [shard_points(pts, r, 8) for r in range(8)]
+    assert sorted(i for d in dealt for i, _ in d) == list(range(64))
+    assert all(len(d) == 8 for d in dealt)
+
+
+def _sweep_worker(rank, world, port, out_q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1012_4382_b200.sweep import run_sweep
+    pts = list(range(11))
+    res = run_sweep(pts, lambda p: (p, p * p, rank), workers=2, dist=dist)
+    out_q.put((rank, res))
+    dist.destroy_process_group()
+
+
+def test_gloo_sweep_gathers_in_point_order():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[1] is None
+    assert [r[:2] for r in res[0]] == [(p, p * p) for p in range(11)]
+    assert {r[2] for r in res[0]} == {0, 1}       # both ranks contributed
