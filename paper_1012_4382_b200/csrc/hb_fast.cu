@@ -1416,14 +1416,232 @@ static cudaError_t mm2_launch(int stage, const KParams& p, cudaStream_t s) {
   return mm2_launch_b<D, KP1, 1>(stage, p, s);
 }
 
+// ---------------------------------------------------------------------------
+// Production kernel (variant 6): k_mm2's 12-pass bookkeeping with the
+// accumulator in registers and predicated gathers.
+//   * The shared-memory accumulator of k_mm2 cost ~700 L1 wavefronts per tile
+//     and stage (ncu: 22-28% of the LSU data pipe); here acc[] lives in
+//     registers: phase A builds it from the ADO (registers) and the TMA'd base
+//     tile, phase B adds the neighbour crosses straight into it, phase C stores
+//     it.  The base tile's shared memory is reused for stage 2's (Y2 - s)/3.
+//   * Absent links (TRUNCATED raise at the top tier, ABSENT lower where
+//     n_m = 0) are predicated off per lane instead of reading a zero tile, so
+//     they generate no L1 wavefronts; with the reference (tier-major) order the
+//     top-tier tiles -- 64% of the ADOs at N_max = 8, K = 1 -- issue no raise
+//     traffic at all, and lower links of a tile land on ~2 lines per request.
+template <int D, int KP1, int STAGE, int MINB>
+__global__ void __launch_bounds__(32, MINB) k_mm3(const KParams P) {
+  constexpr int NP = D * D;
+  constexpr int M = D * KP1;
+  constexpr int TB = NP * TILE;
+  __shared__ __align__(128) double sBase[STAGE >= 2 ? NP : 1][TILE];
+  __shared__ int sU[M][TILE];
+  __shared__ int sD[M][TILE];
+  __shared__ unsigned char sN[M][TILE];
+  __shared__ __align__(8) uint64_t bar;
+
+  volatile Ctl* ctl = P.ctl;
+  if (ctl->status != ST_RUNNING) return;
+  const long long step_next = ctl->step + 1;
+  const int lane = threadIdx.x;
+  const int tile = P.tile_begin + blockIdx.x;
+  const size_t toff = (size_t)tile * TB;
+  const size_t tb = toff + lane;
+  double maxa2 = 0.0;
+  const double c = STAGE == 4 ? P.dt / 6.0 : P.coef;
+
+  if (STAGE >= 2 && lane == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, TB * 8u);
+    bulk_g2s(&sBase[0][0], (STAGE == 4 ? P.Bbuf : P.sig) + toff, TB * 8, &bar);
+  }
+  __syncwarp();
+  // ---- links (element offsets, -1 = absent), n, damping
+  const size_t gb = (size_t)tile * M * TILE + lane;
+  int tk[KP1];
+#pragma unroll
+  for (int k = 0; k < KP1; ++k) tk[k] = 0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int up = __ldg(P.plus + gb + m * TILE);
+    const int dn = __ldg(P.minus + gb + m * TILE);
+    const int n = __ldg(P.nvec + gb + m * TILE);
+    tk[m % KP1] += n;
+    sU[m][lane] = up >= 0 && !P.debug ? (up >> 5) * TB + (up & 31) : -1;
+    sD[m][lane] = dn >= 0 && !P.debug ? (dn >> 5) * TB + (dn & 31) : -1;
+    sN[m][lane] = (unsigned char)n;
+  }
+  double damp = 0.0;  // heom.py:275, generalised: sum_k nu_k * sum_j n_jk
+#pragma unroll
+  for (int k = 0; k < KP1; ++k) damp += (double)tk[k] * P.nu[k];
+
+  double acc[NP];
+  {  // ---- phase A: base + c * (damping + commutator), ADO in registers
+    double s[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) s[p] = __ldg(P.Yin + tb + p * TILE);
+    if (tile == 0 && lane == 0) {  // sink rates of this stage input (heom.py:282-283)
+      int q = 0;
+      for (int sk = 0; sk < P.n_sinks; ++sk) {
+        double a = 0.0;
+        for (int cc = 0; cc < P.sink_nterms[sk]; ++cc, ++q) {
+          const double v = P.sink_rate[q] * __ldg(P.Yin + P.sink_pos[q] * TILE);
+          a = cc == 0 ? v : a + v;
+        }
+        ctl->r[STAGE - 1][sk] = a;
+      }
+    }
+    if (STAGE >= 2) mbar_wait(&bar, 0);
+    auto base = [&](int p) -> double {
+      if (STAGE == 1) return s[p];
+      const double b = sBase[p][lane];
+      if (STAGE == 2) sBase[p][lane] = (s[p] - b) * (1.0 / 3.0);  // park (Y2 - s)/3 for B
+      if (STAGE == 4) return b + s[p] * (1.0 / 3.0);
+      return b;
+    };
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double cm_im = 0.0;
+#pragma unroll
+      for (int l = 0; l < D; ++l)
+        if (l != i) cm_im += P.h[i * MAXD + l] * sim<D>(s, i, l);
+      acc[i] = base(i) + c * (-(damp + P.decay[i]) * s[i] - 2.0 * cm_im);
+#pragma unroll
+      for (int j = i + 1; j < D; ++j) {
+        const int pr = Pk<D>::re(i, j), pim = Pk<D>::im(i, j);
+        const double f = -(damp + 0.5 * (P.decay[i] + P.decay[j]));
+        double cr = 0.0, ci = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+          const double hil = P.h[i * MAXD + l], hlj = P.h[l * MAXD + j];
+          cr += hil * sre<D>(s, l, j) - sre<D>(s, i, l) * hlj;
+          ci += hil * sim<D>(s, l, j) - sim<D>(s, i, l) * hlj;
+        }
+        acc[pr] = base(pr) + c * (f * s[pr] + ci);  // -1j * cm
+        acc[pim] = base(pim) + c * (f * s[pim] - cr);
+      }
+    }
+  }
+  __syncwarp();
+  // ---- phase B: neighbour crosses, one site at a time, predicated per lane
+#pragma unroll
+  for (int st = 0; st < D; ++st) {
+    double cre[D], cim[D];
+#pragma unroll
+    for (int o = 0; o < D; ++o) cre[o] = cim[o] = 0.0;
+#pragma unroll
+    for (int k = 0; k < KP1; ++k) {
+      const int m = st * KP1 + k;
+      const int ou = sU[m][lane], od = sD[m][lane];
+      const bool vu = ou >= 0, vd = od >= 0;
+      const double* up = P.Yin + (vu ? ou : 0);
+      const double* dn = P.Yin + (vd ? od : 0);
+      const double n = (double)sN[m][lane];
+      const double cb = n * P.b[k], ca = n * P.a[k];
+      auto ld = [](const double* q, bool v) {
+        double r = 0.0;
+        if (v) r = __ldg(q);
+        return r;
+      };
+      cre[st] += 2.0 * cb * ld(dn + st * TILE, vd);
+#pragma unroll
+      for (int o = 0; o < D; ++o) {
+        if (o == st) continue;
+        const int a = st < o ? st : o, b = st < o ? o : st;
+        const int pr = Pk<D>::re(a, b), pim = Pk<D>::im(a, b);
+        const double ur = ld(up + pr * TILE, vu), ui = ld(up + pim * TILE, vu);
+        const double dr = ld(dn + pr * TILE, vd), di = ld(dn + pim * TILE, vd);
+        if (o > st) {
+          cre[o] += cb * dr - ca * di - ui;
+          cim[o] += cb * di + ca * dr + ur;
+        } else {
+          cre[o] += cb * dr + ca * di + ui;
+          cim[o] += cb * di - ca * dr - ur;
+        }
+      }
+    }
+    acc[st] += c * cre[st];
+#pragma unroll
+    for (int o = 0; o < D; ++o) {
+      if (o == st) continue;
+      const int a = st < o ? st : o, b = st < o ? o : st;
+      acc[Pk<D>::re(a, b)] += c * cre[o];
+      acc[Pk<D>::im(a, b)] += c * cim[o];
+    }
+  }
+  // ---- phase C: store (stage 2 also B = (Y2 - s)/3 + 2/3 Y3)
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    P.Yout[tb + p * TILE] = acc[p];
+    if (STAGE == 2) P.Bbuf[tb + p * TILE] = sBase[p][lane] + (2.0 / 3.0) * acc[p];
+  }
+  if (STAGE == 4) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      maxa2 = fmax(maxa2, acc[i] * acc[i]);
+#pragma unroll
+      for (int j = i + 1; j < D; ++j) {
+        const double yr = acc[Pk<D>::re(i, j)], yi = acc[Pk<D>::im(i, j)];
+        maxa2 = fmax(maxa2, yr * yr + yi * yi);
+      }
+    }
+    __shared__ int s_last;
+    if (step_next % 25 == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxa2 = fmax(maxa2, __shfl_xor_sync(0xffffffffu, maxa2, o));
+      if (lane == 0)
+        atomicMax(const_cast<unsigned long long*>(&ctl->maxabs2_bits),
+                  (unsigned long long)__double_as_longlong(maxa2));
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      const unsigned prev = atomicAdd(const_cast<unsigned*>(&ctl->blocks_done), 1u);
+      s_last = prev == gridDim.x - 1;
+    }
+    __syncwarp();
+    if (s_last) {
+      __threadfence();
+      if (lane == 0) ctl->launches = ctl->launches + 4;
+      finish_step_warp<D, true>(P, step_next);
+    }
+  }
+}
+
+template <int D, int KP1, int MINB>
+static cudaError_t mm3_launch_b(int stage, const KParams& p, cudaStream_t s) {
+  switch (stage) {
+    case 1: k_mm3<D, KP1, 1, MINB><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 2: k_mm3<D, KP1, 2, MINB><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 3: k_mm3<D, KP1, 3, MINB><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 4: k_mm3<D, KP1, 4, MINB><<<p.n_tiles, 32, 0, s>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <int D, int KP1>
+static cudaError_t mm3_launch(int stage, const KParams& p, cudaStream_t s) {
+  if constexpr (D == 7) {
+    switch (mm2_minb()) {
+      case 10: return mm3_launch_b<D, KP1, 10>(stage, p, s);
+      case 12: return mm3_launch_b<D, KP1, 12>(stage, p, s);
+      case 16: return mm3_launch_b<D, KP1, 16>(stage, p, s);
+      default: break;
+    }
+  }
+  return mm3_launch_b<D, KP1, 1>(stage, p, s);
+}
+
 bool fast_supported(int d, int kp1) { return d >= 1 && d <= 8 && kp1 >= 1 && kp1 <= 2; }
 
-// HB_FAST_VARIANT (experiments): 5 = mode-major + TMA base tile, 12-pass RK (default),
+// HB_FAST_VARIANT (experiments): 6 = register accumulator + predicated gathers (default),
+// 5 = mode-major + TMA base tile, 12-pass RK,
 // 4 = mode-major, 1 = sigma in registers, 3 = TMA, 2 = warp-split, 0 = column-streamed
 static int fast_variant() {
   static int v = [] {
     const char* e = getenv("HB_FAST_VARIANT");
-    return e ? atoi(e) : 5;
+    return e ? atoi(e) : 6;
   }();
   return v;
 }
@@ -1463,6 +1681,7 @@ template <int D, int KP1>
 static cudaError_t fast_dispatch(int stage, const KParams& p, cudaStream_t s) {
   if constexpr (D == 7) {
     const int v = fast_variant();
+    if (v == 6) return mm3_launch<D, KP1>(stage, p, s);
     if (v == 5) return mm2_launch<D, KP1>(stage, p, s);
     if (v == 4) return mm_launch<D, KP1>(stage, p, s);
     if (v != 3) {
@@ -1475,7 +1694,7 @@ static cudaError_t fast_dispatch(int stage, const KParams& p, cudaStream_t s) {
       default: return tma_launch<D, KP1, 8>(stage, p, s);
     }
   } else {  // other d: the production kernel only
-    return mm2_launch<D, KP1>(stage, p, s);
+    return mm3_launch<D, KP1>(stage, p, s);
   }
 }
 
