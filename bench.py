@@ -252,7 +252,9 @@ def run_b200(args):
     from paper_1012_4382_b200.engine import BlockOperands, DeviceRun
     ops = BlockOperands(system, bath, rates, K_MATS)
     n_tot = xf.hierarchy_size(ops.modes, N_MAX)
-    run = DeviceRun(ops, N_MAX, DT, t_end_fs=1e15, record_stride=10 ** 12, device=device)
+    # HB_BENCH_ORDER (experiments): device ADO order of the timed run ('lex' default)
+    run = DeviceRun(ops, N_MAX, DT, t_end_fs=1e15, record_stride=10 ** 12, device=device,
+                    ordering=os.environ.get("HB_BENCH_ORDER", "lex"))
     rho0 = np.zeros((D, D), complex)
     rho0[0, 0] = 1.0
     run.set_rho0(rho0, [0.0, 0.0])

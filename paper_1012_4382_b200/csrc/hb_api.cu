@@ -539,8 +539,10 @@ static int alloc_state(hb_handle* h, int layout) {
   h->base.n_planes = h->n_planes;
   bool identity = h->prm.n_sites == d;
   for (int i = 0; i < d; ++i) identity = identity && h->site_of[i] == i;
+  // the unrolled kernels address a buffer with int32 element offsets
+  const bool fits32 = (h->n_tiles + 1) * (int64_t)TILE * h->n_planes < INT32_MAX;
   h->base.fast = h->base.hermitian && identity && fast_supported(d, h->prm.kp1) &&
-                 h->prm.kernel_variant == HB_KERNEL_AUTO;
+                 h->prm.kernel_variant == HB_KERNEL_AUTO && fits32;
   if (h->base.fast) CK(configure_fast(h->base));
   CK(configure_stages(h->base));
   return HB_OK;

@@ -18,35 +18,11 @@
 #include <cstdlib>
 #include <type_traits>
 #include "hb_device.cuh"
+#include "hb_fast.cuh"
 
 namespace hb {
 
 constexpr int FT = 64;  // threads (ADOs) per CTA
-
-template <int D>
-struct Pk {  // Hermitian packed planes: diagonal i -> i, upper (i<j) -> D + 2*off
-  __host__ __device__ static constexpr int off(int i, int j) {
-    int e = 0;
-    for (int r = 0; r < i; ++r) e += D - 1 - r;
-    return e + (j - i - 1);
-  }
-  __host__ __device__ static constexpr int re(int i, int j) {
-    return i == j ? i : D + 2 * off(i < j ? i : j, i < j ? j : i);
-  }
-  __host__ __device__ static constexpr int im(int i, int j) {
-    return D + 2 * off(i < j ? i : j, i < j ? j : i) + 1;
-  }
-};
-
-// sigma_{ij} from the packed register copy (i, j compile-time after unrolling)
-template <int D>
-__device__ __forceinline__ double sre(const double (&s)[D * D], int i, int j) {
-  return s[Pk<D>::re(i, j)];
-}
-template <int D>
-__device__ __forceinline__ double sim(const double (&s)[D * D], int i, int j) {
-  return i == j ? 0.0 : (i < j ? s[Pk<D>::im(i, j)] : -s[Pk<D>::im(i, j)]);
-}
 
 template <int STAGE>
 __device__ __forceinline__ void epilogue(const KParams& P, size_t tb, int pr, int pim, double sr,
@@ -624,34 +600,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_split(const KParams P) {
 // (the register-fed variants above stay latency bound at ~3 TB/s).  Compute is
 // the warp-split scheme (X = H sigma columns in shared memory, compile-time
 // element sets per warp); only the neighbour gathers remain LDGs.
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "HB_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra HB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 
 template <int D, int KP1, int STAGE>
 struct TmaLayout {
@@ -1635,13 +1583,14 @@ static cudaError_t mm3_launch(int stage, const KParams& p, cudaStream_t s) {
 
 bool fast_supported(int d, int kp1) { return d >= 1 && d <= 8 && kp1 >= 1 && kp1 <= 2; }
 
-// HB_FAST_VARIANT (experiments): 6 = register accumulator + predicated gathers (default),
+// HB_FAST_VARIANT (experiments): 7 = k_mm4 (hb_mm4.cu, default),
+// 6 = register accumulator + predicated gathers,
 // 5 = mode-major + TMA base tile, 12-pass RK,
 // 4 = mode-major, 1 = sigma in registers, 3 = TMA, 2 = warp-split, 0 = column-streamed
 static int fast_variant() {
   static int v = [] {
     const char* e = getenv("HB_FAST_VARIANT");
-    return e ? atoi(e) : 6;
+    return e ? atoi(e) : 7;
   }();
   return v;
 }
@@ -1681,6 +1630,9 @@ template <int D, int KP1>
 static cudaError_t fast_dispatch(int stage, const KParams& p, cudaStream_t s) {
   if constexpr (D == 7) {
     const int v = fast_variant();
+    if (v == 9) return launch_mm6(stage, p, s);
+    if (v == 8) return launch_mm5(stage, p, s);
+    if (v == 7) return launch_mm4(stage, p, s);
     if (v == 6) return mm3_launch<D, KP1>(stage, p, s);
     if (v == 5) return mm2_launch<D, KP1>(stage, p, s);
     if (v == 4) return mm_launch<D, KP1>(stage, p, s);
@@ -1694,7 +1646,7 @@ static cudaError_t fast_dispatch(int stage, const KParams& p, cudaStream_t s) {
       default: return tma_launch<D, KP1, 8>(stage, p, s);
     }
   } else {  // other d: the production kernel only
-    return mm3_launch<D, KP1>(stage, p, s);
+    return launch_mm4(stage, p, s);
   }
 }
 

@@ -96,6 +96,12 @@ struct KParams {
 bool fast_supported(int d, int kp1);
 cudaError_t launch_fast(int stage, const KParams& p, cudaStream_t s);
 cudaError_t configure_fast(const KParams& p);  // before graph capture
+// hb_mm4.cu: production stage kernel (variant 7, default for d <= 8, K+1 <= 2)
+cudaError_t launch_mm4(int stage, const KParams& p, cudaStream_t s);
+// hb_mm5.cu: link-slot-compacted stage kernel (variant 8)
+cudaError_t launch_mm5(int stage, const KParams& p, cudaStream_t s);
+// hb_mm6.cu: persistent contiguous-range stage kernel (variant 9)
+cudaError_t launch_mm6(int stage, const KParams& p, cudaStream_t s);
 
 // hb_stage.cu
 cudaError_t launch_stage(int stage, const KParams& p, cudaStream_t s);

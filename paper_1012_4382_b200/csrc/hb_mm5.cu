@@ -1,0 +1,219 @@
+// Production stage kernel (variant 8, k_mm5): link-slot compaction.
+//
+// A lane's ADO has up to 2M links (raise n+e_m, lower n-e_m), but on average
+// only ~10 of the 28 exist at N_max = 8, K = 1: every raise link of the top
+// tier is TRUNCATED (64% of the ADOs) and a lower link exists only where
+// n_m > 0.  The site-major kernels (k_mm3/k_mm4) walk all 2M slots in 7
+// compile-time rounds and predicate the absent lanes off, so most of their
+// register-resident gather slots carry no bytes and a tile pays 7 L2 round
+// trips.  Here a warp first forms the UNION of its 32 lanes' valid slots with
+// one ballot per slot (warp-uniform bit masks), then walks only those slots in
+// groups of G: each group issues its G x (2d-1) cross loads back to back (one
+// round trip), then adds them into the register accumulator through a
+// warp-uniform switch on (site, direction), whose bodies are compile-time
+// unrolled (plane offsets and signs are immediates).
+//
+// With the tier-major device order (ordering 'reference': tiers contiguous,
+// lexicographic inside a tier) a tile's lanes share their raise validity and
+// mostly their lower-link pattern: the union is ~14.5 slots per tile against
+// 28 (and 22.8 with the pure lexicographic order), ~4 rounds instead of 7.
+//
+// Arithmetic per slot (reference RHS, _kernels.py:41-57, K+1 modes per site;
+// c = RK stage coefficient folded into every coefficient):
+//   raise (site st): row-st element (st,o):    acc += c * (-i) sigma_up(st,o)
+//                    column-st element (o,st): acc += c * (+i) sigma_up(o,st)
+//   lower (site st, mode k, n = n_m):
+//                    row st:    acc += c n (b_k + i a_k) sigma_dn
+//                    column st: acc += c n (b_k - i a_k) sigma_dn
+//                    diagonal:  acc += 2 c n b_k sigma_dn(st,st)
+// Slots are visited in a fixed order (raise modes ascending, then lower), so
+// the result is deterministic and independent of chunking or sharding.
+#include <cstdlib>
+#include "hb_device.cuh"
+#include "hb_fast.cuh"
+#include "hb_mm_common.cuh"
+
+namespace hb {
+
+// element offsets (plane * TILE) of the 2d-1 cross planes of site st:
+// [0] = diagonal (st,st), then (re, im) of (st,o) for o != st ascending
+template <int D>
+struct CrossPlanes {
+  int off[D][2 * D - 1];
+  constexpr CrossPlanes() : off() {
+    for (int st = 0; st < D; ++st) {
+      off[st][0] = Pk<D>::re(st, st) * TILE;
+      int q = 1;
+      for (int o = 0; o < D; ++o) {
+        if (o == st) continue;
+        off[st][q++] = Pk<D>::re(st, o) * TILE;
+        off[st][q++] = Pk<D>::im(st, o) * TILE;
+      }
+    }
+  }
+};
+
+template <int D>
+__constant__ CrossPlanes<D> kCross = CrossPlanes<D>();
+
+// adds one gathered cross (v[0..2D-2]) of site ST into acc; DIR 0 = raise, 1 = lower
+template <int D, int ST, int DIR>
+__device__ __forceinline__ void add_cross(double (&acc)[D * D], const double (&v)[2 * D - 1],
+                                          double cu, double cb, double ca) {
+  if (DIR == 1) acc[ST] = fma(2.0 * cb, v[0], acc[ST]);
+  int q = 1;
+#pragma unroll
+  for (int o = 0; o < D; ++o) {
+    if (o == ST) continue;
+    const int pr = Pk<D>::re(ST, o), pim = Pk<D>::im(ST, o);
+    const double xr = v[q], xi = v[q + 1];
+    q += 2;
+    if (DIR == 0) {
+      if (o > ST) {  // element (st, o): row st, -i x
+        acc[pr] = fma(-cu, xi, acc[pr]);
+        acc[pim] = fma(cu, xr, acc[pim]);
+      } else {       // element (o, st): column st, +i x
+        acc[pr] = fma(cu, xi, acc[pr]);
+        acc[pim] = fma(-cu, xr, acc[pim]);
+      }
+    } else {
+      if (o > ST) {  // (b + i a) x
+        acc[pr] = fma(cb, xr, fma(-ca, xi, acc[pr]));
+        acc[pim] = fma(cb, xi, fma(ca, xr, acc[pim]));
+      } else {       // (b - i a) x
+        acc[pr] = fma(cb, xr, fma(ca, xi, acc[pr]));
+        acc[pim] = fma(cb, xi, fma(-ca, xr, acc[pim]));
+      }
+    }
+  }
+}
+
+template <int D, int ST = 0>
+__device__ __forceinline__ void add_cross_rt(int st, int dir, double (&acc)[D * D],
+                                             const double (&v)[2 * D - 1], double cu, double cb,
+                                             double ca) {
+  if constexpr (ST < D) {
+    if (st == ST) {
+      if (dir == 0) add_cross<D, ST, 0>(acc, v, cu, cb, ca);
+      else add_cross<D, ST, 1>(acc, v, cu, cb, ca);
+    } else {
+      add_cross_rt<D, ST + 1>(st, dir, acc, v, cu, cb, ca);
+    }
+  }
+}
+
+template <int D, int KP1, int STAGE, int G>
+__global__ void __launch_bounds__(32, 1) k_mm5(const KParams P) {
+  constexpr int NP = D * D;
+  constexpr int M = D * KP1;
+  constexpr int TB = NP * TILE;
+  constexpr int NC = 2 * D - 1;
+  static_assert(M <= 16, "slot masks hold 16 modes per direction");
+  __shared__ __align__(128) double sBase[STAGE >= 2 ? NP : 1][TILE];
+  __shared__ __align__(16) int32_t sUp[M][TILE];
+  __shared__ __align__(16) int32_t sDn[M][TILE];
+  __shared__ __align__(16) uint8_t sN[M][TILE];
+  __shared__ __align__(8) uint64_t bar;
+
+  volatile Ctl* ctl = P.ctl;
+  if (ctl->status != ST_RUNNING) return;
+  const long long step_next = ctl->step + 1;
+  const int lane = threadIdx.x;
+  const int tile = P.tile_begin + blockIdx.x;
+  const int own = tile * TB + lane;
+  const double c = STAGE == 4 ? P.dt / 6.0 : P.coef;
+
+  tile_prologue<D, KP1, STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0], &sN[0][0], &bar);
+  double acc[NP];
+  phase_a<D, KP1, STAGE>(P, tile, lane, own, c, sBase, sN, &bar, acc);
+
+  // ---- phase B: the union of the lanes' valid link slots, G per round trip
+  unsigned slots = 0;  // bit m: raise via mode m, bit 16 + m: lower via mode m
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    if (__any_sync(0xffffffffu, sUp[m][lane] >= 0)) slots |= 1u << m;
+    if (__any_sync(0xffffffffu, sDn[m][lane] >= 0)) slots |= 1u << (16 + m);
+  }
+  while (slots) {
+    int sl[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      sl[g] = slots ? __ffs(slots) - 1 : -1;
+      slots &= slots - 1;
+    }
+    double v[G][NC];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (sl[g] < 0) continue;
+      const int m = sl[g] & 15, st = m / KP1;
+      const int raw = sl[g] >= 16 ? sDn[m][lane] : sUp[m][lane];
+      const double* q = P.Yin + ((raw >> 5) * TB + (raw & 31));
+#pragma unroll
+      for (int e = 0; e < NC; ++e) {
+        double x = 0.0;
+        if (raw >= 0) x = __ldg(q + kCross<D>.off[st][e]);
+        v[g][e] = x;
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (sl[g] < 0) continue;
+      const int m = sl[g] & 15, st = m / KP1, k = m % KP1, dir = sl[g] >= 16;
+      const double n = dir ? (double)sN[m][lane] : 0.0;
+      add_cross_rt<D>(st, dir, acc, v[g], c, c * n * P.b[k], c * n * P.a[k]);
+    }
+  }
+  phase_c<D, STAGE>(P, lane, own, step_next, sBase, acc);
+}
+
+template <int D, int KP1, int G>
+static cudaError_t mm5_launch_g(int stage, const KParams& p, cudaStream_t s) {
+  switch (stage) {
+    case 1: k_mm5<D, KP1, 1, G><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 2: k_mm5<D, KP1, 2, G><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 3: k_mm5<D, KP1, 3, G><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 4: k_mm5<D, KP1, 4, G><<<p.n_tiles, 32, 0, s>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <int D, int KP1>
+static cudaError_t mm5_launch_t(int stage, const KParams& p, cudaStream_t s) {
+  // HB_MM5_G (experiments): slots per round trip
+  static const int g = [] {
+    const char* e = getenv("HB_MM5_G");
+    return e ? atoi(e) : 4;
+  }();
+  if constexpr (D == 7 && KP1 == 2) {
+    switch (g) {
+      case 2: return mm5_launch_g<D, KP1, 2>(stage, p, s);
+      case 3: return mm5_launch_g<D, KP1, 3>(stage, p, s);
+      case 5: return mm5_launch_g<D, KP1, 5>(stage, p, s);
+      case 6: return mm5_launch_g<D, KP1, 6>(stage, p, s);
+      default: break;
+    }
+  }
+  return mm5_launch_g<D, KP1, 4>(stage, p, s);
+}
+
+template <int D>
+static cudaError_t mm5_kp1(int stage, const KParams& p, cudaStream_t s) {
+  return p.kp1 == 1 ? mm5_launch_t<D, 1>(stage, p, s) : mm5_launch_t<D, 2>(stage, p, s);
+}
+
+cudaError_t launch_mm5(int stage, const KParams& p, cudaStream_t s) {
+  switch (p.d) {
+    case 1: return mm5_kp1<1>(stage, p, s);
+    case 2: return mm5_kp1<2>(stage, p, s);
+    case 3: return mm5_kp1<3>(stage, p, s);
+    case 4: return mm5_kp1<4>(stage, p, s);
+    case 5: return mm5_kp1<5>(stage, p, s);
+    case 6: return mm5_kp1<6>(stage, p, s);
+    case 7: return mm5_kp1<7>(stage, p, s);
+    case 8: return mm5_kp1<8>(stage, p, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hb
