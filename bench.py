@@ -231,6 +231,7 @@ def run_sharded(args, dist, world, rank, local):
                 "config": {**config_dict(world), "parallelism": f"sharded x{world} (NCCL halo)",
                            "halo_tiles_rank0": halo},
                 "gpu_launches": int(launches),
+            "single_precision": single,
                 "status": status}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -280,14 +281,34 @@ def run_b200(args):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     run.close()
+
+    # same workload with precision='single' (heom.py:74; float32 state, 2,352 B per
+    # ADO-step): reported beside the FP64 headline, not instead of it
+    single = None
+    try:
+        run_s = DeviceRun(ops, N_MAX, DT, t_end_fs=1e15, record_stride=10 ** 12, device=device,
+                          precision="single")
+        run_s.set_rho0(rho0, [0.0, 0.0])
+        run_s.time_steps(max(3, args.warmup))
+        ms_s = run_s.time_steps(args.steps)
+        _, st_s = run_s.time_steps(1, per_stage=True)
+        run_s.close()
+        single = {"value": n_tot * args.steps / (ms_s / 1e3), "unit": UNIT,
+                  "ms_per_step": ms_s / args.steps, "dtype": "f32",
+                  "stage_us": [round(1e3 * x, 2) for x in st_s],
+                  "achieved_GBps": n_tot * B_ALG_STEP / 2 / (float(np.sum(st_s)) / 1e3) / 1e9}
+    except Exception as exc:  # never let the secondary line kill the headline
+        single = {"error": str(exc)}
     # DRAM traffic of the same four stage launches from the committed ncu --set full capture
     traffic = None
+    kname = "stage kernels"
     summ = ROOT / "profiles" / "r1_stage_kernels.json"
     if summ.exists():
         try:
             launches_ = json.loads(summ.read_text())["launches"]
             traffic = sum(e["dram_total_MB"] for e in launches_ if "k_" in e["kernel"]) * 1e6
-        except (KeyError, ValueError):
+            kname = launches_[0]["kernel"]
+        except (KeyError, ValueError, IndexError):
             traffic = None
 
     # end to end: the public API with host buffers (operands + rho0 in, records out)
@@ -325,7 +346,7 @@ def run_b200(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_unit": "DRAM bytes per RK4 step (4 stage launches), ncu",
                          "alg_bytes_per_step": B_ALG_STEP * n_tot,
-                         "kernel": "k_mm2<7,2,stage> (4 launches per RK4 step; achieved = alg bytes / sum of stage times)",
+                         "kernel": f"{kname} .. stage 4 (4 launches per RK4 step; achieved = alg bytes / sum of stage times)",
                          "bytes_per_ado_step": B_ALG_STEP,
                          "stage_us": [round(1e3 * x, 2) for x in stage_ms],
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
@@ -336,6 +357,7 @@ def run_b200(args):
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                     "api": "paper_1012_4382_b200.propagate (t_end run, record_stride=1)"},
             "gpu_launches": int(launches),
+            "single_precision": single,
             "clocks": clk,
             "cpu_baseline": cpu,
         }

@@ -47,6 +47,12 @@ extern "C" {
 #define HB_KERNEL_AUTO 0       /* unrolled thread-per-ADO kernel when the shape allows */
 #define HB_KERNEL_GENERIC 1    /* runtime-shaped tile kernel (any d, K, layout)        */
 
+/* state precision (heom.py:74 PropagationConfig.precision, heom.py:93-94 dtype) */
+#define HB_PREC_DOUBLE 0       /* complex128 state, FP64 arithmetic                     */
+#define HB_PREC_SINGLE 1       /* complex64 state, FP32 RHS arithmetic, FP64 bookkeeping;
+                                  needs the production shape (Hermitian rho0, every block
+                                  level a site, d <= 8, K + 1 <= 2)                     */
+
 #define HB_MAX_D 9
 #define HB_MAX_KP1 8
 #define HB_MAX_SINKS 4
@@ -90,6 +96,7 @@ typedef struct {
     int kernel_variant;       /* HB_KERNEL_*                                      */
     int tile_begin;           /* sharding: first tile (32 ADOs) this handle owns  */
     int tile_count;           /* sharding: tiles owned (0 = all from tile_begin)  */
+    int precision;            /* HB_PREC_*                                        */
 } hb_params;
 
 typedef struct {

@@ -22,6 +22,7 @@ HB_STOP_NONE, HB_STOP_T_END, HB_STOP_RESIDUAL = 0, 1, 2
 HB_LAYOUT = {"auto": 0, "hermitian": 1, "general": 2}
 HB_ORDER = {"lex": 0, "reference": 1}
 HB_KERNEL = {"auto": 0, "generic": 1}
+HB_PREC = {"double": 0, "single": 1}
 
 #: every symbol include/heom_b200.h declares (checked by the CPU test-suite)
 EXPORTS = ("hb_last_error", "hb_device_count", "hb_hierarchy_size", "hb_graph_build",
@@ -44,7 +45,7 @@ class HbParams(C.Structure):
         ("record_stride", C.c_int64), ("record_matrices", C.c_int),
         ("blowup_norm", C.c_double), ("device", C.c_int), ("layout", C.c_int),
         ("ordering", C.c_int), ("chunk_steps", C.c_int), ("kernel_variant", C.c_int),
-        ("tile_begin", C.c_int), ("tile_count", C.c_int),
+        ("tile_begin", C.c_int), ("tile_count", C.c_int), ("precision", C.c_int),
     ]
 
 

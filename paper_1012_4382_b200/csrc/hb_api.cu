@@ -366,6 +366,8 @@ int hb_create(const hb_params* P, hb_handle** out) {
   if (q.d_full > MAXFULL) return fail(HB_ERR_ARG, "full basis dimension above 16 is not supported");
   if (!(q.dt > 0)) return fail(HB_ERR_ARG, "dt must be > 0");
   if (q.record_stride < 1) return fail(HB_ERR_ARG, "record stride must be >= 1");
+  if (q.precision != HB_PREC_DOUBLE && q.precision != HB_PREC_SINGLE)
+    return fail(HB_ERR_ARG, "precision must be 'double' or 'single'");
   int nterms = 0;
   for (int s = 0; s < q.n_sinks; ++s) nterms += q.sink_nterms[s];
   if (nterms > MAXT) return fail(HB_ERR_ARG, "too many sink terms");
@@ -457,6 +459,16 @@ int hb_create(const hb_params* P, hb_handle** out) {
     p.a[k] = h->a[k];
     p.b[k] = h->b[k];
   }
+  // single precision: the RHS operands rounded once, like the reference's float32
+  // h_block / decay / nvec arrays (heom.py:235-275 with rdtype = float32)
+  p.single = q.precision == HB_PREC_SINGLE;
+  for (int i = 0; i < MAXD * MAXD; ++i) p.hf[i] = (float)p.h[i];
+  for (int i = 0; i < MAXD; ++i) p.decayf[i] = (float)p.decay[i];
+  for (int k = 0; k < MAXKP1; ++k) {
+    p.nuf[k] = (float)p.nu[k];
+    p.af[k] = (float)p.a[k];
+    p.bf[k] = (float)p.b[k];
+  }
   p.plus = h->gt.plus_t;
   p.minus = h->gt.minus_t;
   p.nvec = h->gt.nvec_t;
@@ -523,6 +535,9 @@ static KParams stage_params(hb_handle* h, int stage) {
   return p;
 }
 
+// bytes per state element: float for HB_PREC_SINGLE, double otherwise
+static size_t elem_size(const hb_handle* h) { return h->base.single ? sizeof(float) : sizeof(double); }
+
 static int alloc_state(hb_handle* h, int layout) {
   if (h->layout == layout && h->buf[0]) return HB_OK;
   free_state(h);
@@ -530,7 +545,16 @@ static int alloc_state(hb_handle* h, int layout) {
   const int d = h->prm.d;
   h->n_planes = layout == HB_LAYOUT_HERMITIAN ? d * d : 2 * d * d;
   // one extra all-zero tile per buffer: target of absent links (never written)
-  const size_t bytes = (size_t)(h->n_tiles + 1) * TILE * h->n_planes * sizeof(double);
+  if (h->base.single) {
+    bool identity = h->prm.n_sites == d;
+    for (int i = 0; i < d; ++i) identity = identity && h->site_of[i] == i;
+    if (layout != HB_LAYOUT_HERMITIAN || !identity || !fast_supported(d, h->prm.kp1) ||
+        h->prm.kernel_variant != HB_KERNEL_AUTO)
+      return fail(HB_ERR_ARG,
+                  "precision='single' needs a Hermitian rho0, every block level a site, "
+                  "d <= 8, n_matsubara <= 1 and kernel='auto'");
+  }
+  const size_t bytes = (size_t)(h->n_tiles + 1) * TILE * h->n_planes * elem_size(h);
   for (auto& b : h->buf) {
     CK(cudaMalloc(&b, bytes));
     CK(cudaMemsetAsync(b, 0, bytes, h->stream));
@@ -600,7 +624,7 @@ int hb_set_rho0(hb_handle* h, const double* rho0, const double* sink_pops) {
   int rc = alloc_state(h, layout);
   if (rc) return rc;
   // sigma: auxiliaries zero, sigma^0 = rho0 block in tile 0, lane 0
-  const size_t bytes = (size_t)h->n_tiles * TILE * h->n_planes * sizeof(double);
+  const size_t bytes = (size_t)h->n_tiles * TILE * h->n_planes * elem_size(h);
   CK(cudaMemsetAsync(h->buf[0], 0, bytes, h->stream));
   std::vector<double> tile0((size_t)h->n_planes * TILE, 0.0);
   if (layout == HB_LAYOUT_HERMITIAN) {
@@ -618,8 +642,14 @@ int hb_set_rho0(hb_handle* h, const double* rho0, const double* sink_pops) {
       tile0[(size_t)(2 * k + 1) * TILE] = rho0[2 * k + 1];
     }
   }
-  CK(cudaMemcpyAsync(h->buf[0], tile0.data(), tile0.size() * sizeof(double),
-                     cudaMemcpyHostToDevice, h->stream));
+  if (h->base.single) {  // pageable source: the copy is staged before the call returns
+    std::vector<float> tile0f(tile0.begin(), tile0.end());
+    CK(cudaMemcpyAsync(h->buf[0], tile0f.data(), tile0f.size() * sizeof(float),
+                       cudaMemcpyHostToDevice, h->stream));
+  } else {
+    CK(cudaMemcpyAsync(h->buf[0], tile0.data(), tile0.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, h->stream));
+  }
   Ctl c{};
   c.status = ST_RUNNING;
   for (int s = 0; s < h->prm.n_sinks; ++s) c.sink_pops[s] = sink_pops[s];
@@ -725,10 +755,16 @@ int hb_get_sigma0(hb_handle* h, double* sig0, double* sink_pops) {
   CK(cudaSetDevice(h->device));
   const int d = h->prm.d;
   std::vector<double> tile0((size_t)h->n_planes * TILE);
-  CK(cudaMemcpyAsync(tile0.data(), h->buf[0], tile0.size() * sizeof(double),
-                     cudaMemcpyDeviceToHost, h->stream));
+  std::vector<float> tile0f(h->base.single ? tile0.size() : 0);
+  if (h->base.single)
+    CK(cudaMemcpyAsync(tile0f.data(), h->buf[0], tile0f.size() * sizeof(float),
+                       cudaMemcpyDeviceToHost, h->stream));
+  else
+    CK(cudaMemcpyAsync(tile0.data(), h->buf[0], tile0.size() * sizeof(double),
+                       cudaMemcpyDeviceToHost, h->stream));
   int rc = sync_ctl(h);
   if (rc) return rc;
+  if (h->base.single) tile0.assign(tile0f.begin(), tile0f.end());
   auto at = [&](int plane) { return tile0[(size_t)plane * TILE]; };  // lane 0 = ADO 0
   if (h->layout == HB_LAYOUT_HERMITIAN) {
     for (int i = 0; i < d; ++i) {
@@ -840,12 +876,13 @@ int hb_sync(hb_handle* h, int* status, int64_t* step) {
 int hb_copy_tiles(hb_handle* dst, hb_handle* src, int buf, int first_tile, int n_tiles) {
   if (!dst || !src || !dst->ready || !src->ready) return fail(HB_ERR_ARG, "handles not ready");
   if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
-  if (dst->n_planes != src->n_planes || dst->n_tiles != src->n_tiles)
+  if (dst->n_planes != src->n_planes || dst->n_tiles != src->n_tiles ||
+      dst->base.single != src->base.single)
     return fail(HB_ERR_ARG, "handles have different layouts");
   if (first_tile < 0 || n_tiles < 0 || first_tile + n_tiles > dst->n_tiles)
     return fail(HB_ERR_ARG, "tile range outside the hierarchy");
   if (n_tiles == 0) return HB_OK;
-  const size_t tb = (size_t)TILE * dst->n_planes * sizeof(double);
+  const size_t tb = (size_t)TILE * dst->n_planes * elem_size(dst);
   cudaEvent_t ev;
   CK(cudaSetDevice(src->device));
   CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -941,7 +978,7 @@ int hb_exchange(hb_handle* h, int buf, int n, const int32_t* peer, const int32_t
   if (!h || !h->ready || !h->nccl_comm) return fail(HB_ERR_ARG, "handle without NCCL communicator");
   if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
   CK(cudaSetDevice(h->device));
-  const size_t tb = (size_t)TILE * h->n_planes * sizeof(double);
+  const size_t tb = (size_t)TILE * h->n_planes * elem_size(h);
   int r = nccl().group_start();
   if (r) return nccl_fail(r, "ncclGroupStart");
   for (int i = 0; i < n; ++i) {

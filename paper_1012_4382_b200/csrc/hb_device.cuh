@@ -65,7 +65,25 @@ __device__ __forceinline__ void plane_info(int p, int& i, int& j, int& part) {
 
 // sigma^0 entry (i, j) straight from global memory (tile 0, lane 0)
 template <int D, bool HERM>
-__device__ __forceinline__ void load_sig0(const double* s, int i, int j, double& re, double& im) {
+__device__ __forceinline__ void load_sig0(const double* s, int i, int j, double& re, double& im,
+                                          bool single = false) {
+  if (single) {  // float state (HB_PREC_SINGLE): Hermitian-packed only
+    const float* f = reinterpret_cast<const float*>(s);
+    if (i == j) {
+      re = (double)__ldcg(f + i * TILE);
+      im = 0.0;
+      return;
+    }
+    const int a = i < j ? i : j, b = i < j ? j : i;
+    int e = D;
+    for (int r = 0; r < a; ++r) e += D - 1 - r;
+    e += b - a - 1;
+    const int pr = D + 2 * (e - D);
+    re = (double)__ldcg(f + pr * TILE);
+    im = (double)__ldcg(f + (pr + 1) * TILE);
+    if (i > j) im = -im;
+    return;
+  }
   if (HERM) {
     if (i == j) {
       re = __ldcg(s + i * TILE);
@@ -149,7 +167,8 @@ struct Sig0 {
 template <int D, bool HERM>
 __device__ void sig0_warp(const KParams& P, Sig0& s0) {
   const int lane = threadIdx.x & 31;
-  for (int f = lane; f < D * D; f += 32) load_sig0<D, HERM>(P.sig, f / D, f % D, s0.re[f], s0.im[f]);
+  for (int f = lane; f < D * D; f += 32)
+    load_sig0<D, HERM>(P.sig, f / D, f % D, s0.re[f], s0.im[f], P.single != 0);
   __syncwarp();
 }
 

@@ -1656,6 +1656,7 @@ static cudaError_t fast_kp1(int stage, const KParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_fast(int stage, const KParams& p, cudaStream_t s) {
+  if (p.single) return launch_mm4(stage, p, s);  // the float state has one kernel
   switch (p.d) {
     case 1: return fast_kp1<1>(stage, p, s);
     case 2: return fast_kp1<2>(stage, p, s);

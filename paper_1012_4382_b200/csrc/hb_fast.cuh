@@ -22,13 +22,21 @@ struct Pk {  // Hermitian packed planes: diagonal i -> i, upper (i<j) -> D + 2*o
 };
 
 // sigma_{ij} from the packed register copy (i, j compile-time after unrolling)
+template <class T, int D>
+__device__ __forceinline__ T sre(const T (&s)[D * D], int i, int j) {
+  return s[Pk<D>::re(i, j)];
+}
+template <class T, int D>
+__device__ __forceinline__ T sim(const T (&s)[D * D], int i, int j) {
+  return i == j ? (T)0 : (i < j ? s[Pk<D>::im(i, j)] : -s[Pk<D>::im(i, j)]);
+}
 template <int D>
 __device__ __forceinline__ double sre(const double (&s)[D * D], int i, int j) {
-  return s[Pk<D>::re(i, j)];
+  return sre<double, D>(s, i, j);
 }
 template <int D>
 __device__ __forceinline__ double sim(const double (&s)[D * D], int i, int j) {
-  return i == j ? 0.0 : (i < j ? s[Pk<D>::im(i, j)] : -s[Pk<D>::im(i, j)]);
+  return sim<double, D>(s, i, j);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

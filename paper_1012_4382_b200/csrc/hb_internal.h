@@ -64,6 +64,9 @@ struct KParams {
   int prefetch;              // bulk-prefetch epilogue tiles into L2 at kernel start
   int pf_dist;               // L2 prefetch distance in tiles (0 = off)
   int debug;                 // timing experiments only (HB_DEBUG_NOGATHER): links -> zero tile
+  int single;                // HB_PREC_SINGLE: the state buffers hold float (production
+                             // kernel only); the operands below in float for its RHS
+  float hf[MAXD * MAXD], decayf[MAXD], nuf[MAXKP1], af[MAXKP1], bf[MAXKP1];
   double coef;               // dt/2, dt/2, dt for stages 1-3
   double dt;
   // bookkeeping

@@ -10,13 +10,15 @@
 //     RK stage coefficient c is folded into the link coefficients once per link
 //     (c*n*b_k, c*n*a_k, and c for a raise link), so nothing is scaled twice;
 //   * an absent link (TRUNCATED raise at the top tier, ABSENT lower where
-//     n_m = 0) is redirected to the lane's OWN ADO (an L1 hit, loaded in phase
-//     A) with coefficient 0 -- no zeroing moves, no zero tile, no L2 traffic;
+//     n_m = 0) is predicated off (measured: redirecting it to the own ADO with
+//     a zero coefficient, or prefetching the next site into L1, is slower);
 //   * the tile's base operand (sigma, or B at stage 4) and its three link
 //     tables ([mode][32] int32 raise/lower, uint8 n) arrive by one bulk copy
 //     group (cp.async.bulk, one mbarrier) at kernel start: no per-lane table
 //     LDG/STS round trip, the raw positions are decoded to element offsets
 //     where they are used.
+// T = double (HB_PREC_DOUBLE) or float (HB_PREC_SINGLE: float state, float RHS,
+// heom.py:93-94; bookkeeping, sinks and records stay double).
 // The arithmetic is the reference RHS (_kernels.py:23-58 generalised to K+1
 // modes per site); the stage combinations are k_mm2's (hb_fast.cu):
 //   stage 1: Y2 = s + h/2 k1;  2: Y3 = s + h/2 k2, B = (Y2 - s)/3 + 2/3 Y3;
@@ -28,22 +30,16 @@
 
 namespace hb {
 
-__device__ __forceinline__ void pf_l1(const double* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-
-// VAR (experiments, HB_MM4_VAR): bit 0 = predicate absent links off (zero) instead
-// of redirecting them to the own ADO; bit 1 = prefetch the next site's crosses
-// into L1 while the current site is gathered; bit 2 = skip the neighbour
-// crosses (timing experiment only, wrong results).
-template <int D, int KP1, int STAGE, int MINB, int VAR>
-__global__ void __launch_bounds__(32, MINB) k_mm4(const KParams P) {
-  constexpr bool kPred = VAR & 1, kPf = VAR & 2, kNoB = VAR & 4;
+// VAR (experiments, HB_MM4_VAR): 1 = production; 5 = skip the neighbour crosses
+// (timing experiment for the streamed part alone; wrong results).
+template <class T, int D, int KP1, int STAGE, int VAR>
+__global__ void __launch_bounds__(32, 1) k_mm4(const KParams P) {
   constexpr int NP = D * D;
   constexpr int M = D * KP1;
   constexpr int TB = NP * TILE;
-  constexpr bool kBase = STAGE >= 2;
-  __shared__ __align__(128) double sBase[kBase ? NP : 1][TILE];
+  constexpr bool kInc = kIncScheme<T>;
+  __shared__ __align__(128) T sBase[STAGE >= 2 || kInc ? NP : 1][TILE];
+  __shared__ __align__(128) T sInc[kInc && (STAGE == 2 || STAGE == 4) ? NP : 1][TILE];
   __shared__ __align__(16) int32_t sUp[M][TILE];
   __shared__ __align__(16) int32_t sDn[M][TILE];
   __shared__ __align__(16) uint8_t sN[M][TILE];
@@ -54,112 +50,40 @@ __global__ void __launch_bounds__(32, MINB) k_mm4(const KParams P) {
   const long long step_next = ctl->step + 1;
   const int lane = threadIdx.x;
   const int tile = P.tile_begin + blockIdx.x;
-  const size_t toff = (size_t)tile * TB;
-  const int own = (int)toff + lane;  // element offset of this lane's ADO, plane 0
-  const double c = STAGE == 4 ? P.dt / 6.0 : P.coef;
+  const int own = tile * TB + lane;  // element offset of this lane's ADO, plane 0
+  const T c = (T)(STAGE == 4 ? P.dt / 6.0 : P.coef);
 
-  tile_prologue<D, KP1, STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0], &sN[0][0], &bar);
-
-  double acc[NP];
-  phase_a<D, KP1, STAGE>(P, tile, lane, own, c, sBase, sN, &bar, acc);
-  // ---- phase B: neighbour crosses, one site at a time, straight into acc
-  double cbk[KP1], cak[KP1];
-#pragma unroll
-  for (int k = 0; k < KP1; ++k) {
-    cbk[k] = c * P.b[k];
-    cak[k] = c * P.a[k];
-  }
-  auto prefetch_site = [&](int st) {
-#pragma unroll
-    for (int k = 0; k < KP1; ++k) {
-      const int m = st * KP1 + k;
-      const int pu = sUp[m][lane], pd = sDn[m][lane];
-      const double* up = P.Yin + ((pu >> 5) * TB + (pu & 31));
-      const double* dn = P.Yin + ((pd >> 5) * TB + (pd & 31));
-#pragma unroll
-      for (int o = 0; o < D; ++o) {
-        const int pr = Pk<D>::re(st, o);
-        if (pd >= 0) pf_l1(dn + pr * TILE);
-        if (o != st && pu >= 0) pf_l1(up + pr * TILE);
-        if (o != st) {
-          const int pim = Pk<D>::im(st, o);
-          if (pd >= 0) pf_l1(dn + pim * TILE);
-          if (pu >= 0) pf_l1(up + pim * TILE);
-        }
-      }
-    }
-  };
-  if (kPf) prefetch_site(0);
-#pragma unroll
-  for (int st = 0; st < (kNoB ? 0 : D); ++st) {
-    if (kPf && st + 1 < D) prefetch_site(st + 1);
-#pragma unroll
-    for (int k = 0; k < KP1; ++k) {
-      const int m = st * KP1 + k;
-      const int pu = sUp[m][lane], pd = sDn[m][lane];
-      const bool vu = pu >= 0, vd = pd >= 0;
-      const double* up = P.Yin + (vu ? (pu >> 5) * TB + (pu & 31) : own);
-      const double* dn = P.Yin + (vd ? (pd >> 5) * TB + (pd & 31) : own);
-      const double n = vd ? (double)sN[m][lane] : 0.0;
-      const double cb = n * cbk[k], ca = n * cak[k];
-      const double cu = vu ? c : 0.0;
-      auto ld = [&](const double* q, bool v) -> double {
-        if (!kPred) return __ldg(q);
-        double r = 0.0;
-        if (v) r = __ldg(q);
-        return r;
-      };
-      acc[st] = fma(2.0 * cb, ld(dn + st * TILE, vd), acc[st]);
-#pragma unroll
-      for (int o = 0; o < D; ++o) {
-        if (o == st) continue;
-        const int pr = Pk<D>::re(st, o), pim = Pk<D>::im(st, o);
-        const double ur = ld(up + pr * TILE, vu), ui = ld(up + pim * TILE, vu);
-        const double dr = ld(dn + pr * TILE, vd), di = ld(dn + pim * TILE, vd);
-        if (o > st) {  // element (st, o): row st
-          acc[pr] = fma(cb, dr, fma(-ca, di, fma(-cu, ui, acc[pr])));
-          acc[pim] = fma(cb, di, fma(ca, dr, fma(cu, ur, acc[pim])));
-        } else {       // element (o, st): column st
-          acc[pr] = fma(cb, dr, fma(ca, di, fma(cu, ui, acc[pr])));
-          acc[pim] = fma(cb, di, fma(-ca, dr, fma(-cu, ur, acc[pim])));
-        }
-      }
-    }
-  }
-  phase_c<D, STAGE>(P, lane, own, step_next, sBase, acc);
+  tile_prologue<T, D, KP1, STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0], &sN[0][0], &bar,
+                                  true, &sInc[0][0]);
+  T acc[NP];
+  phase_a<T, D, KP1, STAGE>(P, tile, lane, own, c, sBase, sN, &bar, acc);
+  if (VAR != 5) phase_b_sites<T, D, KP1>(P, lane, c, sUp, sDn, sN, acc);
+  phase_c<T, D, STAGE>(P, lane, own, step_next, sBase, acc, sInc);
 }
 
-template <int D, int KP1, int MINB, int VAR>
+template <class T, int D, int KP1, int VAR>
 static cudaError_t mm4_launch_b(int stage, const KParams& p, cudaStream_t s) {
   switch (stage) {
-    case 1: k_mm4<D, KP1, 1, MINB, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
-    case 2: k_mm4<D, KP1, 2, MINB, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
-    case 3: k_mm4<D, KP1, 3, MINB, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
-    case 4: k_mm4<D, KP1, 4, MINB, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 1: k_mm4<T, D, KP1, 1, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 2: k_mm4<T, D, KP1, 2, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 3: k_mm4<T, D, KP1, 3, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 4: k_mm4<T, D, KP1, 4, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
 template <int D, int KP1>
 static cudaError_t mm4_launch_t(int stage, const KParams& p, cudaStream_t s) {
-  // HB_MM4_VAR (experiments): see k_mm4's VAR bits
-  static const int var = env_int("HB_MM4_VAR", 1);
-  if constexpr (D == 7) {
-    switch (var) {
-      case 0: return mm4_launch_b<D, KP1, 1, 0>(stage, p, s);
-      case 1: return mm4_launch_b<D, KP1, 1, 1>(stage, p, s);
-      case 2: return mm4_launch_b<D, KP1, 1, 2>(stage, p, s);
-      case 5: return mm4_launch_b<D, KP1, 1, 5>(stage, p, s);
-      default: break;
-    }
+  if (p.single) return mm4_launch_b<float, D, KP1, 1>(stage, p, s);
+  if constexpr (D == 7 && KP1 == 2) {
+    static const int var = [] {
+      const char* e = getenv("HB_MM4_VAR");
+      return e ? atoi(e) : 1;
+    }();
+    if (var == 5) return mm4_launch_b<double, D, KP1, 5>(stage, p, s);
   }
-  return mm4_launch_b<D, KP1, 1, 3>(stage, p, s);
+  return mm4_launch_b<double, D, KP1, 1>(stage, p, s);
 }
 
 template <int D>

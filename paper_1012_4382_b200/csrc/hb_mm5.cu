@@ -123,9 +123,9 @@ __global__ void __launch_bounds__(32, 1) k_mm5(const KParams P) {
   const int own = tile * TB + lane;
   const double c = STAGE == 4 ? P.dt / 6.0 : P.coef;
 
-  tile_prologue<D, KP1, STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0], &sN[0][0], &bar);
+  tile_prologue<double, D, KP1, STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0], &sN[0][0], &bar);
   double acc[NP];
-  phase_a<D, KP1, STAGE>(P, tile, lane, own, c, sBase, sN, &bar, acc);
+  phase_a<double, D, KP1, STAGE>(P, tile, lane, own, c, sBase, sN, &bar, acc);
 
   // ---- phase B: the union of the lanes' valid link slots, G per round trip
   unsigned slots = 0;  // bit m: raise via mode m, bit 16 + m: lower via mode m
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(32, 1) k_mm5(const KParams P) {
       add_cross_rt<D>(st, dir, acc, v[g], c, c * n * P.b[k], c * n * P.a[k]);
     }
   }
-  phase_c<D, STAGE>(P, lane, own, step_next, sBase, acc);
+  phase_c<double, D, STAGE>(P, lane, own, step_next, sBase, acc);
 }
 
 template <int D, int KP1, int G>

@@ -58,12 +58,12 @@ __global__ void __launch_bounds__(32 * W, 1) k_mm6(const KParams P) {
   for (int t = t0 + w; t < t1; t += W, ++it) {
     const int tile = P.tile_begin + t;
     const int own = tile * TB + lane;
-    tile_prologue<D, KP1, STAGE>(P, tile, &sBase[w][0][0], &sUp[w][0][0], &sDn[w][0][0],
+    tile_prologue<double, D, KP1, STAGE>(P, tile, &sBase[w][0][0], &sUp[w][0][0], &sDn[w][0][0],
                                  &sN[w][0][0], &bar[w], it == 0);
     double acc[NP];
-    phase_a<D, KP1, STAGE>(P, tile, lane, own, c, sBase[w], sN[w], &bar[w], acc, it & 1u);
-    phase_b_sites<D, KP1>(P, lane, c, sUp[w], sDn[w], sN[w], acc);
-    phase_c_store<D, STAGE>(P, lane, own, sBase[w], acc, maxa2);
+    phase_a<double, D, KP1, STAGE>(P, tile, lane, own, c, sBase[w], sN[w], &bar[w], acc, it & 1u);
+    phase_b_sites<double, D, KP1>(P, lane, c, sUp[w], sDn[w], sN[w], acc);
+    phase_c_store<double, D, STAGE>(P, lane, own, sBase[w], acc, maxa2);
     __syncwarp();  // every lane done with this tile's shared memory before the refill
   }
   if (STAGE == 4) stage4_finish<D>(P, step_next, maxa2);

@@ -7,23 +7,70 @@
 //                     of the stage input (heom.py:282-283) on tile 0;
 //   phase_c        -- store (stage 2 also B), stage-4 max|x|^2 and the
 //                     last-CTA step bookkeeping (heom.py:381-394).
-// The stage combinations (12 state passes per step) are k_mm2's (hb_fast.cu).
+// The stage combinations (12 state passes per step) are k_mm2's (hb_fast.cu) for
+// T = double.  For T = float (precision='single') that scheme's differences of
+// rounded stage values ((Y2 - s)/3 ...) cost several float ulps of sigma per step,
+// so the float path carries the RK increment instead (kInc, 15 float passes):
+//   stage 1: Y2 = s + a1,          Binc = a1 / 3            (a1 = h/2 k1)
+//   stage 2: Y3 = s + a2,          Binc += 2/3 a2           (a2 = h/2 k2)
+//   stage 3: Y4 = s + a3                                    (a3 = h k3)
+//   stage 4: s  = s + (Binc + a4 + (Y4 - s)/3)             (a4 = h/6 k4)
+// acc holds the increment a_s (never the rounded sum), so sigma is rounded once
+// per step like the reference's rk4_update (_kernels.py:68-72, heom.py:381).
 #pragma once
+#include <type_traits>
 #include "hb_device.cuh"
 #include "hb_fast.cuh"
 
 namespace hb {
+
+// operands in the kernel's arithmetic type (HB_PREC_SINGLE: float copies in KParams)
+template <class T> struct Opd;
+template <> struct Opd<double> {
+  static __device__ __forceinline__ double h(const KParams& P, int i) { return P.h[i]; }
+  static __device__ __forceinline__ double decay(const KParams& P, int i) { return P.decay[i]; }
+  static __device__ __forceinline__ double nu(const KParams& P, int k) { return P.nu[k]; }
+  static __device__ __forceinline__ double a(const KParams& P, int k) { return P.a[k]; }
+  static __device__ __forceinline__ double b(const KParams& P, int k) { return P.b[k]; }
+};
+template <> struct Opd<float> {
+  static __device__ __forceinline__ float h(const KParams& P, int i) { return P.hf[i]; }
+  static __device__ __forceinline__ float decay(const KParams& P, int i) { return P.decayf[i]; }
+  static __device__ __forceinline__ float nu(const KParams& P, int k) { return P.nuf[k]; }
+  static __device__ __forceinline__ float a(const KParams& P, int k) { return P.af[k]; }
+  static __device__ __forceinline__ float b(const KParams& P, int k) { return P.bf[k]; }
+};
+// state buffers of the stage (KParams keeps them as double*; float when single)
+template <class T> __device__ __forceinline__ const T* st_in(const KParams& P) {
+  return reinterpret_cast<const T*>(P.Yin);
+}
+template <class T> __device__ __forceinline__ T* st_out(const KParams& P) {
+  return reinterpret_cast<T*>(P.Yout);
+}
+template <class T> __device__ __forceinline__ T* st_b(const KParams& P) {
+  return reinterpret_cast<T*>(P.Bbuf);
+}
+template <class T> __device__ __forceinline__ const T* st_sig(const KParams& P) {
+  return reinterpret_cast<const T*>(P.sig);
+}
 
 template <int D, int KP1>
 struct MmSmem {
   static constexpr int NP = D * D, M = D * KP1;
 };
 
-template <int D, int KP1, int STAGE>
-__device__ __forceinline__ void tile_prologue(const KParams& P, int tile, double* sBase,
+// float state: increment scheme (see the header)
+template <class T>
+constexpr bool kIncScheme = std::is_same<T, float>::value;
+
+template <class T, int D, int KP1, int STAGE>
+__device__ __forceinline__ void tile_prologue(const KParams& P, int tile, T* sBase,
                                               int32_t* sUp, int32_t* sDn, uint8_t* sN,
-                                              uint64_t* bar, bool init = true) {
+                                              uint64_t* bar, bool init = true,
+                                              T* sInc = nullptr) {
   constexpr int NP = D * D, M = D * KP1, TB = NP * TILE;
+  constexpr bool kInc = kIncScheme<T>;
+  constexpr bool kLoadInc = kInc && (STAGE == 2 || STAGE == 4);
   if ((threadIdx.x & 31) == 0) {
     constexpr unsigned LB = M * TILE * 4u, NB = M * TILE;
     if (init) {
@@ -31,12 +78,16 @@ __device__ __forceinline__ void tile_prologue(const KParams& P, int tile, double
     } else {  // the warp's generic-proxy reads of the previous tile precede the refill
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    mbar_expect_tx(bar, 2 * LB + NB + (STAGE >= 2 ? TB * 8u : 0u));
+    mbar_expect_tx(bar, 2 * LB + NB + (STAGE >= 2 ? TB * (unsigned)sizeof(T) : 0u) +
+                            (kLoadInc ? TB * (unsigned)sizeof(T) : 0u));
     const size_t gt = (size_t)tile * M * TILE;
     bulk_g2s(sUp, P.plus + gt, LB, bar);
     bulk_g2s(sDn, P.minus + gt, LB, bar);
     bulk_g2s(sN, P.nvec + gt, NB, bar);
-    if (STAGE >= 2) bulk_g2s(sBase, (STAGE == 4 ? P.Bbuf : P.sig) + (size_t)tile * TB, TB * 8u, bar);
+    if (STAGE >= 2)
+      bulk_g2s(sBase, (STAGE == 4 && !kInc ? st_b<T>(P) : st_sig<T>(P)) + (size_t)tile * TB,
+               TB * (unsigned)sizeof(T), bar);
+    if (kLoadInc) bulk_g2s(sInc, st_b<T>(P) + (size_t)tile * TB, TB * (unsigned)sizeof(T), bar);
   }
   __syncwarp();  // barrier initialised before any lane waits on it
 }
@@ -44,17 +95,17 @@ __device__ __forceinline__ void tile_prologue(const KParams& P, int tile, double
 // status: the run's status read at kernel start (its load overlaps the tile's);
 // returns false -- after draining the bulk copy, before any global write --
 // when the run is no longer RUNNING (graph replays past the stop are no-ops)
-template <int D, int KP1, int STAGE>
-__device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, int own, double c,
-                                        double (*sBase)[TILE], const uint8_t (*sN)[TILE],
-                                        uint64_t* bar, double (&acc)[D * D],
+template <class T, int D, int KP1, int STAGE>
+__device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, int own, T c,
+                                        T (*sBase)[TILE], const uint8_t (*sN)[TILE],
+                                        uint64_t* bar, T (&acc)[D * D],
                                         unsigned parity = 0, int status = ST_RUNNING) {
   constexpr int NP = D * D, M = D * KP1;
   volatile Ctl* ctl = P.ctl;
   {  // ---- phase A: base + c * (damping + commutator), ADO in registers
-    double s[NP];
+    T s[NP];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) s[p] = __ldg(P.Yin + own + p * TILE);
+    for (int p = 0; p < NP; ++p) s[p] = __ldg(st_in<T>(P) + own + p * TILE);
     if (status != ST_RUNNING) {
       mbar_wait(bar, parity);
       return false;
@@ -64,7 +115,7 @@ __device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, in
       for (int sk = 0; sk < P.n_sinks; ++sk) {
         double a = 0.0;
         for (int cc = 0; cc < P.sink_nterms[sk]; ++cc, ++q) {
-          const double v = P.sink_rate[q] * __ldg(P.Yin + P.sink_pos[q] * TILE);
+          const double v = P.sink_rate[q] * (double)__ldg(st_in<T>(P) + P.sink_pos[q] * TILE);
           a = cc == 0 ? v : a + v;
         }
         ctl->r[STAGE - 1][sk] = a;
@@ -77,43 +128,50 @@ __device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, in
     for (int k = 0; k < KP1; ++k) tk[k] = 0;
 #pragma unroll
     for (int m = 0; m < M; ++m) tk[m % KP1] += sN[m][lane];
-    double damp = 0.0;
+    T damp = 0;
 #pragma unroll
-    for (int k = 0; k < KP1; ++k) damp = fma((double)tk[k], P.nu[k], damp);
-    auto base = [&](int p) -> double {
+    for (int k = 0; k < KP1; ++k) damp = fma((T)tk[k], Opd<T>::nu(P, k), damp);
+    constexpr T third = (T)(1.0 / 3.0);
+    auto base = [&](int p) -> T {
+      if (kIncScheme<T>) {  // acc = increment; sigma kept (stage 1) or TMA'd in sBase
+        if (STAGE == 1) sBase[p][lane] = s[p];
+        if (STAGE == 4) return (s[p] - sBase[p][lane]) * third;  // (Y4 - s)/3
+        return (T)0;
+      }
       if (STAGE == 1) return s[p];
-      const double b = sBase[p][lane];
-      if (STAGE == 2) sBase[p][lane] = (s[p] - b) * (1.0 / 3.0);  // park (Y2 - s)/3 for B
-      if (STAGE == 4) return fma(s[p], 1.0 / 3.0, b);
+      const T b = sBase[p][lane];
+      if (STAGE == 2) sBase[p][lane] = (s[p] - b) * third;  // park (Y2 - s)/3 for B
+      if (STAGE == 4) return fma(s[p], third, b);
       return b;
     };
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       // diagonal: Re(-i[H,s])_ii = 2 sum_{l != i} h_il Im s_il
-      double cm = 0.0;
+      T cm = 0;
 #pragma unroll
       for (int l = 0; l < D; ++l)
-        if (l != i) cm = fma(P.h[i * MAXD + l], sim<D>(s, i, l), cm);
-      const double fi = -(damp + P.decay[i]);
-      acc[i] = fma(c, fma(fi, s[i], -2.0 * cm), base(i));
+        if (l != i) cm = fma(Opd<T>::h(P, i * MAXD + l), sim<T, D>(s, i, l), cm);
+      const T fi = -(damp + Opd<T>::decay(P, i));
+      acc[i] = fma(c, fma(fi, s[i], (T)-2 * cm), base(i));
 #pragma unroll
       for (int j = i + 1; j < D; ++j) {
         const int pr = Pk<D>::re(i, j), pim = Pk<D>::im(i, j);
         // [H,s]_ij = sum_l h_il s_lj - s_il h_lj; the l = i and l = j terms pair up:
         // (h_ii - h_jj) s_ij + h_ij (s_jj - s_ii)  (s_ii, s_jj real)
-        const double dh = P.h[i * MAXD + i] - P.h[j * MAXD + j], hij = P.h[i * MAXD + j];
-        double cr = fma(hij, s[j], fma(-hij, s[i], dh * s[pr]));
-        double ci = dh * s[pim];
+        const T dh = Opd<T>::h(P, i * MAXD + i) - Opd<T>::h(P, j * MAXD + j);
+        const T hij = Opd<T>::h(P, i * MAXD + j);
+        T cr = fma(hij, s[j], fma(-hij, s[i], dh * s[pr]));
+        T ci = dh * s[pim];
 #pragma unroll
         for (int l = 0; l < D; ++l) {
           if (l == i || l == j) continue;
-          const double hil = P.h[i * MAXD + l], hlj = P.h[l * MAXD + j];
-          cr = fma(hil, sre<D>(s, l, j), cr);
-          cr = fma(-hlj, sre<D>(s, i, l), cr);
-          ci = fma(hil, sim<D>(s, l, j), ci);
-          ci = fma(-hlj, sim<D>(s, i, l), ci);
+          const T hil = Opd<T>::h(P, i * MAXD + l), hlj = Opd<T>::h(P, l * MAXD + j);
+          cr = fma(hil, sre<T, D>(s, l, j), cr);
+          cr = fma(-hlj, sre<T, D>(s, i, l), cr);
+          ci = fma(hil, sim<T, D>(s, l, j), ci);
+          ci = fma(-hlj, sim<T, D>(s, i, l), ci);
         }
-        const double f = -(damp + 0.5 * (P.decay[i] + P.decay[j]));
+        const T f = -(damp + (T)0.5 * (Opd<T>::decay(P, i) + Opd<T>::decay(P, j)));
         acc[pr] = fma(c, fma(f, s[pr], ci), base(pr));   // -1j * [H,s]
         acc[pim] = fma(c, fma(f, s[pim], -cr), base(pim));
       }
@@ -125,17 +183,18 @@ __device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, in
 // phase B: the neighbour crosses, one site at a time (2(K+1) links, 2d-1 planes
 // each, all loads of a site independent), absent links predicated off, every
 // term one DFMA into the register accumulator (c folded into the coefficients)
-template <int D, int KP1>
-__device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, double c,
+template <class T, int D, int KP1>
+__device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
                                               const int32_t (*sUp)[TILE],
                                               const int32_t (*sDn)[TILE],
-                                              const uint8_t (*sN)[TILE], double (&acc)[D * D]) {
+                                              const uint8_t (*sN)[TILE], T (&acc)[D * D]) {
   constexpr int TB = D * D * TILE;
-  double cbk[KP1], cak[KP1];
+  const T* yin = st_in<T>(P);
+  T cbk[KP1], cak[KP1];
 #pragma unroll
   for (int k = 0; k < KP1; ++k) {
-    cbk[k] = c * P.b[k];
-    cak[k] = c * P.a[k];
+    cbk[k] = c * Opd<T>::b(P, k);
+    cak[k] = c * Opd<T>::a(P, k);
   }
 #pragma unroll
   for (int st = 0; st < D; ++st) {
@@ -144,23 +203,23 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, double
       const int m = st * KP1 + k;
       const int pu = sUp[m][lane], pd = sDn[m][lane];
       const bool vu = pu >= 0, vd = pd >= 0;
-      const double* up = P.Yin + ((pu >> 5) * TB + (pu & 31));
-      const double* dn = P.Yin + ((pd >> 5) * TB + (pd & 31));
-      const double n = vd ? (double)sN[m][lane] : 0.0;
-      const double cb = n * cbk[k], ca = n * cak[k];
-      const double cu = vu ? c : 0.0;
-      auto ld = [](const double* q, bool v) -> double {
-        double r = 0.0;
+      const T* up = yin + ((pu >> 5) * TB + (pu & 31));
+      const T* dn = yin + ((pd >> 5) * TB + (pd & 31));
+      const T n = vd ? (T)sN[m][lane] : (T)0;
+      const T cb = n * cbk[k], ca = n * cak[k];
+      const T cu = vu ? c : (T)0;
+      auto ld = [](const T* q, bool v) -> T {
+        T r = 0;
         if (v) r = __ldg(q);
         return r;
       };
-      acc[st] = fma(2.0 * cb, ld(dn + st * TILE, vd), acc[st]);
+      acc[st] = fma((T)2 * cb, ld(dn + st * TILE, vd), acc[st]);
 #pragma unroll
       for (int o = 0; o < D; ++o) {
         if (o == st) continue;
         const int pr = Pk<D>::re(st, o), pim = Pk<D>::im(st, o);
-        const double ur = ld(up + pr * TILE, vu), ui = ld(up + pim * TILE, vu);
-        const double dr = ld(dn + pr * TILE, vd), di = ld(dn + pim * TILE, vd);
+        const T ur = ld(up + pr * TILE, vu), ui = ld(up + pim * TILE, vu);
+        const T dr = ld(dn + pr * TILE, vd), di = ld(dn + pim * TILE, vd);
         if (o > st) {  // element (st, o): row st
           acc[pr] = fma(cb, dr, fma(-ca, di, fma(-cu, ui, acc[pr])));
           acc[pim] = fma(cb, di, fma(ca, dr, fma(cu, ur, acc[pim])));
@@ -173,21 +232,30 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, double
   }
 }
 
-template <int D, int STAGE>
+template <class T, int D, int STAGE>
 __device__ __forceinline__ void phase_c_store(const KParams& P, int lane, int own,
-                                              double (*sBase)[TILE], const double (&acc)[D * D],
-                                              double& maxa2) {
+                                              T (*sBase)[TILE], T (&acc)[D * D],
+                                              double& maxa2, T (*sInc)[TILE] = nullptr) {
   constexpr int NP = D * D;
-  // ---- phase C: store (stage 2 also B = (Y2 - s)/3 + 2/3 Y3)
+  constexpr T third = (T)(1.0 / 3.0), two3 = (T)(2.0 / 3.0);
+  // ---- phase C: store (stage 2 also B = (Y2 - s)/3 + 2/3 Y3; float: see header)
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
-    P.Yout[own + p * TILE] = acc[p];
-    if (STAGE == 2) P.Bbuf[own + p * TILE] = fma(2.0 / 3.0, acc[p], sBase[p][lane]);
+    if (kIncScheme<T>) {
+      const T a = acc[p], sg = sBase[p][lane];
+      if (STAGE == 1) st_b<T>(P)[own + p * TILE] = a * third;
+      if (STAGE == 2) st_b<T>(P)[own + p * TILE] = fma(two3, a, sInc[p][lane]);
+      acc[p] = STAGE == 4 ? sg + (sInc[p][lane] + a) : sg + a;
+      st_out<T>(P)[own + p * TILE] = acc[p];
+    } else {
+      st_out<T>(P)[own + p * TILE] = acc[p];
+      if (STAGE == 2) st_b<T>(P)[own + p * TILE] = fma(two3, acc[p], sBase[p][lane]);
+    }
   }
   if (STAGE == 4) {  // max |y|^2 per element (diagonal planes are real)
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      maxa2 = fmax(maxa2, acc[i] * acc[i]);
+      maxa2 = fmax(maxa2, (double)acc[i] * (double)acc[i]);
 #pragma unroll
       for (int j = i + 1; j < D; ++j) {
         const double yr = acc[Pk<D>::re(i, j)], yi = acc[Pk<D>::im(i, j)];
@@ -225,11 +293,12 @@ __device__ __forceinline__ void stage4_finish(const KParams& P, long long step_n
   }
 }
 
-template <int D, int STAGE>
+template <class T, int D, int STAGE>
 __device__ __forceinline__ void phase_c(const KParams& P, int lane, int own, long long step_next,
-                                        double (*sBase)[TILE], const double (&acc)[D * D]) {
+                                        T (*sBase)[TILE], T (&acc)[D * D],
+                                        T (*sInc)[TILE] = nullptr) {
   double maxa2 = 0.0;
-  phase_c_store<D, STAGE>(P, lane, own, sBase, acc, maxa2);
+  phase_c_store<T, D, STAGE>(P, lane, own, sBase, acc, maxa2, sInc);
   if (STAGE == 4) stage4_finish<D>(P, step_next, maxa2);
 }
 

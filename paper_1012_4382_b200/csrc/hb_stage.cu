@@ -283,11 +283,14 @@ __global__ void k_unpack(const KParams P, const double* __restrict__ src, const 
   const int e = idx % (D * D);
   const int i = e / D, j = e % D;
   const int64_t k = dev2ref[r];
-  const double* s = src + (r >> 5) * Lay<D, HERM>::NP * TILE + (r & 31);
+  const int64_t s0 = (r >> 5) * Lay<D, HERM>::NP * TILE + (r & 31);
+  auto s = [&](int64_t off) -> double {  // float state when HB_PREC_SINGLE
+    return P.single ? (double)reinterpret_cast<const float*>(src)[s0 + off] : src[s0 + off];
+  };
   double re, im;
   if (HERM) {
     if (i == j) {
-      re = s[i * TILE];
+      re = s(i * TILE);
       im = 0.0;
     } else {
       const int a = i < j ? i : j, b = i < j ? j : i;
@@ -295,13 +298,13 @@ __global__ void k_unpack(const KParams P, const double* __restrict__ src, const 
       for (int rr = 0; rr < a; ++rr) ee += D - 1 - rr;
       ee += b - a - 1;
       const int pr = D + 2 * (ee - D);
-      re = s[pr * TILE];
-      im = s[(pr + 1) * TILE];
+      re = s(pr * TILE);
+      im = s((pr + 1) * TILE);
       if (i > j) im = -im;
     }
   } else {
-    re = s[(2 * e) * TILE];
-    im = s[(2 * e + 1) * TILE];
+    re = s((2 * e) * TILE);
+    im = s((2 * e + 1) * TILE);
   }
   ref[(k * D * D + e) * 2] = re;
   ref[(k * D * D + e) * 2 + 1] = im;

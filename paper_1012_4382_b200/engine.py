@@ -113,7 +113,7 @@ class DeviceRun:
                  residual=None, hard_cap_fs: float = 200_000.0, record_stride: int = 1,
                  record_matrices: bool = False, blowup_norm: float = 1e6, device: int = 0,
                  layout: str = "auto", ordering: str = "lex", chunk_steps: int = 0,
-                 kernel: str = "auto", tile_range=None):
+                 kernel: str = "auto", tile_range=None, precision: str = "double"):
         N.require_device(device)
         if ops.d > 9:
             raise ValueError("block dimension above 9 is not supported by the device kernels")
@@ -154,6 +154,7 @@ class DeviceRun:
         p.ordering = N.HB_ORDER[ordering]
         p.chunk_steps = int(chunk_steps)
         p.kernel_variant = N.HB_KERNEL[kernel]
+        p.precision = N.HB_PREC[precision]
         if tile_range is not None:  # sharding (shard.py): owned tiles [begin, begin + count)
             p.tile_begin, p.tile_count = int(tile_range[0]), int(tile_range[1])
         self._params = p

@@ -52,6 +52,11 @@ class PropagationConfig:
       chunk_steps  RK4 steps per CUDA-graph launch (0 = library default);
       kernel       'auto' (unrolled thread-per-ADO kernel when the shape allows)
                    or 'generic' (runtime-shaped tile kernel).
+    ``precision='single'`` (reference field, heom.py:74) runs a float32 state with
+    float32 right-hand sides on the device; sinks, records and the stop policy
+    stay float64.  It needs the production shape: an exactly Hermitian rho0,
+    every block level a site, d <= 8, n_matsubara <= 1, kernel='auto'
+    (otherwise ValueError).
     """
 
     dt_fs: float = 2.5
@@ -252,8 +257,6 @@ def propagate_from(system: ExcitonSystem, bath: BathParams, rates: MarkovRates,
     for s in ops.sinks:
         if any(rho0[s, j] != 0 for j in range(d) if j != s):  # row only, as heom.py:303-305
             raise ValueError("initial state must not carry sink coherences")
-    if config.precision != "double":
-        raise NotImplementedError("precision='single' is not built yet (DESIGN.md, next rows)")
     block = rho0[np.ix_(ops.block, ops.block)]
     if config.layout == "hermitian" and not np.array_equal(block, block.conj().T):
         raise ValueError("layout='hermitian' needs an exactly Hermitian rho0")
@@ -262,7 +265,7 @@ def propagate_from(system: ExcitonSystem, bath: BathParams, rates: MarkovRates,
                     record_stride=config.record_stride, record_matrices=config.record_matrices,
                     blowup_norm=config.blowup_norm, device=config.device, layout=config.layout,
                     ordering=config.ordering, chunk_steps=config.chunk_steps,
-                    kernel=config.kernel)
+                    kernel=config.kernel, precision=config.precision)
     with run:
         run.set_rho0(block, [float(rho0[s, s].real) for s in ops.sinks])
         rc = run.run()

@@ -10,6 +10,7 @@ Usage (from the repo root):
     NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONPATH=/root/reference/pkg/src \
         python tests/golden/make_golden.py            # fast fixtures (~1 min)
     ... make_golden.py --long                          # + the 300 K N_max=6 eta run (~5 min)
+    ... make_golden.py --single                        # only the precision='single' runs
 
 Every fixture records which reference call produced it (`source` key).
 """
@@ -255,11 +256,43 @@ def trajectories(long: bool):
     (OUT / "traj.json").write_text(json.dumps(meta, indent=1))
 
 
+def single_precision():
+    """precision='single' (complex64 state, heom.py:93-94): the reference's own
+    smoke case (test_heom.py:353-360), config 2 and a residual/eta run, each with
+    its double twin, so the suite can check single vs reference-single and the
+    reference's single-vs-double bound (5e-7, test_acceptance.py:231-238)."""
+    arrays, meta = {}, {"source": "excitonflow.heom.propagate, precision='single' (heom.py:74, 93-94)"}
+    fmo = xf.build_fmo_system()
+    rates = xf.MarkovRates.from_inverse_ps(2.5, 250.0)
+    bath300 = xf.BathParams.from_timescale(35.0, 166.0, 300.0)
+    bath77 = xf.BathParams.from_timescale(35.0, 166.0, 77.0)
+    cases = {
+        "smoke_n4": (bath300, dict(dt_fs=10.0, n_max=4, t_end_fs=1000.0, residual=None,
+                                   record_stride=10)),
+        "fmo_n4_77k": (bath77, dict(dt_fs=2.5, n_max=4, t_end_fs=1000.0, residual=None,
+                                    record_stride=20)),
+        "fmo_n2_eta": (bath300, dict(dt_fs=5.0, n_max=2, residual=1e-3, record_stride=20)),
+    }
+    for name, (bath, kw) in cases.items():
+        for prec in ("single", "double"):
+            traj = xf.propagate(fmo, bath, rates, xf.PropagationConfig(precision=prec, **kw), 1)
+            key = f"{name}_{prec}"
+            arrays[key + "_times"] = traj.times_fs
+            arrays[key + "_pops"] = traj.populations
+            meta[key] = {"stop_reason": traj.stop_reason, "eta": float(xf.efficiency(traj))}
+    np.savez_compressed(OUT / "traj_single.npz", **arrays)
+    (OUT / "traj_single.json").write_text(json.dumps(meta, indent=1))
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--single", action="store_true", help="only the precision='single' runs")
     ap.add_argument("--long", action="store_true", help="only the N_max=6 eta run")
     ap.add_argument("--dense", action="store_true", help="only the dense heom_rhs fixtures")
     args = ap.parse_args()
+    if args.single:
+        single_precision()
+        return
     if args.dense:
         dense_cases()
         return
@@ -270,6 +303,7 @@ def main():
     rhs_cases()
     dense_cases()
     trajectories(long=False)
+    single_precision()
 
 
 if __name__ == "__main__":
