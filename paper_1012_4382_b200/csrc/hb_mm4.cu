@@ -61,13 +61,24 @@ __global__ void __launch_bounds__(32, 1) k_mm4(const KParams P) {
   phase_c<T, D, STAGE>(P, lane, own, step_next, sBase, acc, sInc);
 }
 
+// HB_MM4_PAD (experiments): unused dynamic shared memory per CTA, to lower the
+// resident warps per SM (occupancy-sensitivity measurements)
+static int mm4_pad() {
+  static const int v = [] {
+    const char* e = getenv("HB_MM4_PAD");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <class T, int D, int KP1, int VAR>
 static cudaError_t mm4_launch_b(int stage, const KParams& p, cudaStream_t s) {
+  const int pad = mm4_pad();
   switch (stage) {
-    case 1: k_mm4<T, D, KP1, 1, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
-    case 2: k_mm4<T, D, KP1, 2, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
-    case 3: k_mm4<T, D, KP1, 3, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
-    case 4: k_mm4<T, D, KP1, 4, VAR><<<p.n_tiles, 32, 0, s>>>(p); break;
+    case 1: k_mm4<T, D, KP1, 1, VAR><<<p.n_tiles, 32, pad, s>>>(p); break;
+    case 2: k_mm4<T, D, KP1, 2, VAR><<<p.n_tiles, 32, pad, s>>>(p); break;
+    case 3: k_mm4<T, D, KP1, 3, VAR><<<p.n_tiles, 32, pad, s>>>(p); break;
+    case 4: k_mm4<T, D, KP1, 4, VAR><<<p.n_tiles, 32, pad, s>>>(p); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -1,5 +1,6 @@
-// Production stage kernel (variant 9, k_mm6): k_mm4's arithmetic in a
-// persistent CTA per SM that walks a CONTIGUOUS tile range.
+// Experimental stage kernel (variant 9, k_mm6): k_mm4's arithmetic in CTAs of
+// W warps that own a CONTIGUOUS tile range (HB_MM6_R tiles per warp, or
+// persistent: one CTA per SM).
 //
 // The no-gather timing experiment (k_mm4 VAR 5, profiles/) put the streamed
 // part of a step at the HBM floor (0.26 ms) and the neighbour gathers at
@@ -34,7 +35,7 @@ struct Mm6Smem {
 };
 
 template <int D, int KP1, int STAGE, int W>
-__global__ void __launch_bounds__(32 * W, 1) k_mm6(const KParams P) {
+__global__ void __launch_bounds__(32 * W, 8 / W) k_mm6(const KParams P) {
   constexpr int NP = D * D;
   constexpr int M = D * KP1;
   constexpr int TB = NP * TILE;
@@ -88,10 +89,17 @@ static cudaError_t mm6_go(int grid, const KParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 template <int D, int KP1, int W>
 static cudaError_t mm6_launch_w(int stage, const KParams& p, cudaStream_t s) {
-  // one CTA per SM, at most one tile per warp
-  const int grid = std::max(1, std::min(num_sms(), (p.n_tiles + W - 1) / W));
+  // HB_MM6_R (experiments): tiles per warp; 0 = persistent, one CTA per SM
+  static const int r = env_int("HB_MM6_R", 1);
+  const int grid = r > 0 ? std::max(1, (p.n_tiles + W * r - 1) / (W * r))
+                         : std::max(1, std::min(num_sms(), (p.n_tiles + W - 1) / W));
   switch (stage) {
     case 1: return mm6_go<D, KP1, 1, W>(grid, p, s);
     case 2: return mm6_go<D, KP1, 2, W>(grid, p, s);
@@ -103,7 +111,13 @@ static cudaError_t mm6_launch_w(int stage, const KParams& p, cudaStream_t s) {
 
 template <int D, int KP1>
 static cudaError_t mm6_launch_t(int stage, const KParams& p, cudaStream_t s) {
-  return mm6_launch_w<D, KP1, 8>(stage, p, s);
+  // HB_MM6_W (experiments): warps (adjacent tiles) per CTA
+  static const int w = env_int("HB_MM6_W", 4);
+  if constexpr (D == 7 && KP1 == 2) {
+    if (w == 2) return mm6_launch_w<D, KP1, 2>(stage, p, s);
+    if (w == 8) return mm6_launch_w<D, KP1, 8>(stage, p, s);
+  }
+  return mm6_launch_w<D, KP1, 4>(stage, p, s);
 }
 
 template <int D>
