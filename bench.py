@@ -19,6 +19,7 @@ OpenMP over all host cores) on the same workload; the reference itself
 from __future__ import annotations
 
 import argparse
+from dataclasses import replace
 import json
 import os
 import statistics
@@ -41,6 +42,7 @@ S_PACKED = 8 * D * D                      # bytes per Hermitian-packed ADO (392 
 B_ALG_STEP = 12 * S_PACKED                # algorithmic state bytes per ADO-step
 B_ALG_STAGE = {1: 2 * S_PACKED, 2: 4 * S_PACKED, 3: 3 * S_PACKED, 4: 3 * S_PACKED}
 SURVEY_B_ALG = 16 * 16 * D * D            # SURVEY 8(d) unpacked-scheme figure, 12,544 B
+B_ALG_SINGLE = 15 * 4 * D * D             # precision='single': 15 float passes
 
 
 def workload():
@@ -232,6 +234,7 @@ def run_sharded(args, dist, world, rank, local):
                            "halo_tiles_rank0": halo},
                 "gpu_launches": int(launches),
             "single_precision": single,
+            "eta_wall": eta or None,
                 "status": status}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -296,7 +299,8 @@ def run_b200(args):
         single = {"value": n_tot * args.steps / (ms_s / 1e3), "unit": UNIT,
                   "ms_per_step": ms_s / args.steps, "dtype": "f32",
                   "stage_us": [round(1e3 * x, 2) for x in st_s],
-                  "achieved_GBps": n_tot * B_ALG_STEP / 2 / (float(np.sum(st_s)) / 1e3) / 1e9}
+                  "bytes_per_ado_step": B_ALG_SINGLE,
+                  "achieved_GBps": n_tot * B_ALG_SINGLE / (float(np.sum(st_s)) / 1e3) / 1e9}
     except Exception as exc:  # never let the secondary line kill the headline
         single = {"error": str(exc)}
     # DRAM traffic of the same four stage launches from the committed ncu --set full capture
@@ -329,6 +333,26 @@ def run_b200(args):
     h2d = (D * D * 16 + 16 * 4 * D + 64 * D + 512) / e2e_steps  # rho0 tile, operands, ctl
     d2h = traj.populations.shape[1] * 8 + 8 + 256                  # one record + status per step
 
+    # FMO eta wall-time (BASELINE metric, configs[2]): trap + sinks at 300 K, residual
+    # 1e-5 policy, through propagate(); K=1 N_max=6 (38,760 ADOs) and the K=0 twin
+    # whose reference run is in tests/golden/traj_long.json
+    eta = {}
+    if not args.no_eta:
+        for tag, (nm, K, dtf) in {"k1_nmax6": (6, 1, 1.25), "k0_nmax6": (6, 0, 2.5)}.items():
+            cfg_e = xf.PropagationConfig(dt_fs=dtf, n_max=nm, residual=1e-5, record_stride=100,
+                                         n_matsubara=K, device=device)
+            xf.propagate(system, bath, rates, replace(cfg_e, residual=None, t_end_fs=10 * dtf), 1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tr = xf.propagate(system, bath, rates, cfg_e, 1)
+            w = time.perf_counter() - t0
+            eta[tag] = {"eta": float(xf.efficiency(tr)), "wall_s": w,
+                        "steps": int(round(tr.times_fs[-1] / dtf)), "dt_fs": dtf,
+                        "n_ado": xf.hierarchy_size(7 * (K + 1), nm)}
+        eta["reference_k0_nmax6"] = {"eta": 0.9761164832557473, "wall_s": 298.1,
+                                     "note": "reference propagate, 1 thread, measured in the "
+                                             "build container (SURVEY 8(d).3)"}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -358,6 +382,7 @@ def run_b200(args):
                     "api": "paper_1012_4382_b200.propagate (t_end run, record_stride=1)"},
             "gpu_launches": int(launches),
             "single_precision": single,
+            "eta_wall": eta or None,
             "clocks": clk,
             "cpu_baseline": cpu,
         }
@@ -374,6 +399,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-eta", action="store_true", help="skip the config-3 eta wall-time runs")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: split ONE hierarchy across the ranks (NCCL halo exchange) "
                          "instead of independent replicas")

@@ -10,13 +10,13 @@ O=gpurun_out
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $O/smi.txt
 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest=$?" | tee -a $O/pytest_gpu.log
-python bench.py --steps 20 --warmup 20 --no-cpu-baseline "$@" > /dev/null 2>&1; echo "plain=$?"
+python bench.py --steps 20 --warmup 20 --no-cpu-baseline --no-eta "$@" > /dev/null 2>&1; echo "plain=$?"
 ncu --metrics gpu__time_duration.sum --clock-control none -s 80 -c 40 --csv \
-    --log-file $O/launches.csv python bench.py --steps 20 --warmup 20 --no-cpu-baseline "$@" > $O/ncu1.log 2>&1
+    --log-file $O/launches.csv python bench.py --steps 20 --warmup 20 --no-cpu-baseline --no-eta "$@" > $O/ncu1.log 2>&1
 echo "ncu1=$?"
-python bench.py --steps 3 --warmup 20 --no-cpu-baseline "$@" > /dev/null 2>&1; echo "plain2=$?"
+python bench.py --steps 3 --warmup 20 --no-cpu-baseline --no-eta "$@" > /dev/null 2>&1; echo "plain2=$?"
 ncu --set full --clock-control none --import-source on -k regex:$K -s 80 -c 4 -o $O/prof \
-    python bench.py --steps 3 --warmup 20 --no-cpu-baseline "$@" > $O/ncu2.log 2>&1
+    python bench.py --steps 3 --warmup 20 --no-cpu-baseline --no-eta "$@" > $O/ncu2.log 2>&1
 echo "ncu2=$?"
 ncu -i $O/prof.ncu-rep --page raw --csv > $O/prof_raw.csv 2>/dev/null
 ncu -i $O/prof.ncu-rep --page details --csv > $O/prof_details.csv 2>/dev/null
