@@ -46,15 +46,23 @@ __global__ void __launch_bounds__(32, 1) k_mm4(const KParams P) {
   __shared__ __align__(8) uint64_t bar;
 
   volatile Ctl* ctl = P.ctl;
-  if (ctl->status != ST_RUNNING) return;
-  const long long step_next = ctl->step + 1;
   const int lane = threadIdx.x;
   const int tile = P.tile_begin + blockIdx.x;
   const int own = tile * TB + lane;  // element offset of this lane's ADO, plane 0
   const T c = (T)(STAGE == 4 ? P.dt / 6.0 : P.coef);
 
+  // operands no running kernel writes, before the grid dependency (PDL, see
+  // hb_mm_common.cuh); the float increment tile (written by stage 1) after it
   tile_prologue<T, D, KP1, STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0], &sN[0][0], &bar,
-                                  true, &sInc[0][0]);
+                                  true, &sInc[0][0], true);
+  pdl_wait();
+  tile_prologue_late<T, D, STAGE>(P, tile, &sInc[0][0], &bar);
+  if (ctl->status != ST_RUNNING) {
+    mbar_wait(&bar, 0);  // no bulk copy may land after the CTA has exited
+    return;
+  }
+  pdl_release();
+  const long long step_next = ctl->step + 1;
   T acc[NP];
   phase_a<T, D, KP1, STAGE>(P, tile, lane, own, c, sBase, sN, &bar, acc);
   if (VAR != 5) phase_b_sites<T, D, KP1>(P, lane, c, sUp, sDn, sN, acc);
@@ -71,17 +79,39 @@ static int mm4_pad() {
   return v;
 }
 
+// HB_PDL (experiments): 0 disables programmatic dependent launch
+static bool mm4_pdl() {
+  static const bool v = [] {
+    const char* e = getenv("HB_PDL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
+template <class T, int D, int KP1, int STAGE, int VAR>
+static cudaError_t mm4_go(const KParams& p, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.n_tiles);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = (size_t)mm4_pad();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = mm4_pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_mm4<T, D, KP1, STAGE, VAR>, p);
+}
+
 template <class T, int D, int KP1, int VAR>
 static cudaError_t mm4_launch_b(int stage, const KParams& p, cudaStream_t s) {
-  const int pad = mm4_pad();
   switch (stage) {
-    case 1: k_mm4<T, D, KP1, 1, VAR><<<p.n_tiles, 32, pad, s>>>(p); break;
-    case 2: k_mm4<T, D, KP1, 2, VAR><<<p.n_tiles, 32, pad, s>>>(p); break;
-    case 3: k_mm4<T, D, KP1, 3, VAR><<<p.n_tiles, 32, pad, s>>>(p); break;
-    case 4: k_mm4<T, D, KP1, 4, VAR><<<p.n_tiles, 32, pad, s>>>(p); break;
-    default: return cudaErrorInvalidValue;
+    case 1: return mm4_go<T, D, KP1, 1, VAR>(p, s);
+    case 2: return mm4_go<T, D, KP1, 2, VAR>(p, s);
+    case 3: return mm4_go<T, D, KP1, 3, VAR>(p, s);
+    case 4: return mm4_go<T, D, KP1, 4, VAR>(p, s);
   }
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 template <int D, int KP1>

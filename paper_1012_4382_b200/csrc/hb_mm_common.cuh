@@ -67,7 +67,7 @@ template <class T, int D, int KP1, int STAGE>
 __device__ __forceinline__ void tile_prologue(const KParams& P, int tile, T* sBase,
                                               int32_t* sUp, int32_t* sDn, uint8_t* sN,
                                               uint64_t* bar, bool init = true,
-                                              T* sInc = nullptr) {
+                                              T* sInc = nullptr, bool defer_inc = false) {
   constexpr int NP = D * D, M = D * KP1, TB = NP * TILE;
   constexpr bool kInc = kIncScheme<T>;
   constexpr bool kLoadInc = kInc && (STAGE == 2 || STAGE == 4);
@@ -87,9 +87,32 @@ __device__ __forceinline__ void tile_prologue(const KParams& P, int tile, T* sBa
     if (STAGE >= 2)
       bulk_g2s(sBase, (STAGE == 4 && !kInc ? st_b<T>(P) : st_sig<T>(P)) + (size_t)tile * TB,
                TB * (unsigned)sizeof(T), bar);
-    if (kLoadInc) bulk_g2s(sInc, st_b<T>(P) + (size_t)tile * TB, TB * (unsigned)sizeof(T), bar);
+    if (kLoadInc && !defer_inc)
+      bulk_g2s(sInc, st_b<T>(P) + (size_t)tile * TB, TB * (unsigned)sizeof(T), bar);
   }
   __syncwarp();  // barrier initialised before any lane waits on it
+}
+
+// the increment tile copy held back by tile_prologue(defer_inc): issued once the
+// kernel that writes it (stage 1 of the float scheme) is known to be complete
+template <class T, int D, int STAGE>
+__device__ __forceinline__ void tile_prologue_late(const KParams& P, int tile, T* sInc,
+                                                   uint64_t* bar) {
+  constexpr int TB = D * D * TILE;
+  if (kIncScheme<T> && (STAGE == 2 || STAGE == 4) && (threadIdx.x & 31) == 0)
+    bulk_g2s(sInc, st_b<T>(P) + (size_t)tile * TB, TB * (unsigned)sizeof(T), bar);
+}
+
+// Programmatic dependent launch (PDL).  A stage kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while the previous
+// stage's last wave drains: it issues the bulk copies of operands no running
+// kernel writes (link tables; sigma, or B at stage 4, whose writers finished two
+// launches back), then waits for the previous grid to complete and flush
+// (griddepcontrol.wait) before touching its stage input or the control block,
+// and releases its own dependent right after that wait.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // status: the run's status read at kernel start (its load overlaps the tile's);
