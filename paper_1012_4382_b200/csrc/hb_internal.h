@@ -105,6 +105,8 @@ cudaError_t launch_mm4(int stage, const KParams& p, cudaStream_t s);
 cudaError_t launch_mm5(int stage, const KParams& p, cudaStream_t s);
 // hb_mm6.cu: persistent contiguous-range stage kernel (variant 9)
 cudaError_t launch_mm6(int stage, const KParams& p, cudaStream_t s);
+// hb_mm8.cu: TMEM-accumulator stage kernel (variant 11, d = 7, K + 1 = 2)
+cudaError_t launch_mm8(int stage, const KParams& p, cudaStream_t s);
 
 // hb_stage.cu
 cudaError_t launch_stage(int stage, const KParams& p, cudaStream_t s);

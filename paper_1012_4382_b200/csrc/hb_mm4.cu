@@ -31,14 +31,17 @@
 namespace hb {
 
 // VAR (experiments, HB_MM4_VAR): 1 = production; 5 = skip the neighbour crosses
-// (timing experiment for the streamed part alone; wrong results).
+// (timing experiment for the streamed part alone; wrong results); 6 = production
+// with an idle second warp per CTA (half the resident working warps, same L1);
+// 7 = base operands read in phase C instead of bulk-copied to shared memory.
 template <class T, int D, int KP1, int STAGE, int VAR>
-__global__ void __launch_bounds__(32, 1) k_mm4(const KParams P) {
+__global__ void __launch_bounds__(VAR == 6 ? 64 : 32, 1) k_mm4(const KParams P) {
   constexpr int NP = D * D;
   constexpr int M = D * KP1;
   constexpr int TB = NP * TILE;
   constexpr bool kInc = kIncScheme<T>;
-  __shared__ __align__(128) T sBase[STAGE >= 2 || kInc ? NP : 1][TILE];
+  constexpr bool kLate = VAR == 7 && !kInc;  // base operands in phase C (no smem tile)
+  __shared__ __align__(128) T sBase[(STAGE >= 2 && !kLate) || kInc ? NP : 1][TILE];
   __shared__ __align__(128) T sInc[kInc && (STAGE == 2 || STAGE == 4) ? NP : 1][TILE];
   __shared__ __align__(16) int32_t sUp[M][TILE];
   __shared__ __align__(16) int32_t sDn[M][TILE];
@@ -46,6 +49,13 @@ __global__ void __launch_bounds__(32, 1) k_mm4(const KParams P) {
   __shared__ __align__(8) uint64_t bar;
 
   volatile Ctl* ctl = P.ctl;
+  if (VAR == 6 && threadIdx.x >= 32) {  // occupancy experiment: an idle 2nd warp
+    if (STAGE == 4) {
+      pdl_wait();
+      if (ctl->status == ST_RUNNING) stage4_finish<D>(P, ctl->step + 1, 0.0);
+    }
+    return;
+  }
   const int lane = threadIdx.x;
   const int tile = P.tile_begin + blockIdx.x;
   const int own = tile * TB + lane;  // element offset of this lane's ADO, plane 0
@@ -53,8 +63,8 @@ __global__ void __launch_bounds__(32, 1) k_mm4(const KParams P) {
 
   // operands no running kernel writes, before the grid dependency (PDL, see
   // hb_mm_common.cuh); the float increment tile (written by stage 1) after it
-  tile_prologue<T, D, KP1, STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0], &sN[0][0], &bar,
-                                  true, &sInc[0][0], true);
+  tile_prologue<T, D, KP1, kLate ? 1 : STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0],
+                                               &sN[0][0], &bar, true, &sInc[0][0], true);
   pdl_wait();
   tile_prologue_late<T, D, STAGE>(P, tile, &sInc[0][0], &bar);
   if (ctl->status != ST_RUNNING) {
@@ -64,9 +74,11 @@ __global__ void __launch_bounds__(32, 1) k_mm4(const KParams P) {
   pdl_release();
   const long long step_next = ctl->step + 1;
   T acc[NP];
-  phase_a<T, D, KP1, STAGE>(P, tile, lane, own, c, sBase, sN, &bar, acc);
+  phase_a<T, D, KP1, STAGE, kLate>(P, tile, lane, own, c, sBase, sN, &bar, acc);
   if (VAR != 5) phase_b_sites<T, D, KP1>(P, lane, c, sUp, sDn, sN, acc);
-  phase_c<T, D, STAGE>(P, lane, own, step_next, sBase, acc, sInc);
+  double maxa2 = 0.0;
+  phase_c_store<T, D, STAGE, kLate>(P, lane, own, sBase, acc, maxa2, sInc);
+  if (STAGE == 4) stage4_finish<D>(P, step_next, maxa2);
 }
 
 // HB_MM4_PAD (experiments): unused dynamic shared memory per CTA, to lower the
@@ -92,7 +104,7 @@ template <class T, int D, int KP1, int STAGE, int VAR>
 static cudaError_t mm4_go(const KParams& p, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.n_tiles);
-  cfg.blockDim = dim3(32);
+  cfg.blockDim = dim3(VAR == 6 ? 64 : 32);
   cfg.dynamicSmemBytes = (size_t)mm4_pad();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -123,6 +135,8 @@ static cudaError_t mm4_launch_t(int stage, const KParams& p, cudaStream_t s) {
       return e ? atoi(e) : 1;
     }();
     if (var == 5) return mm4_launch_b<double, D, KP1, 5>(stage, p, s);
+    if (var == 6) return mm4_launch_b<double, D, KP1, 6>(stage, p, s);
+    if (var == 7) return mm4_launch_b<double, D, KP1, 7>(stage, p, s);
   }
   return mm4_launch_b<double, D, KP1, 1>(stage, p, s);
 }

@@ -118,7 +118,10 @@ __device__ __forceinline__ void pdl_release() {
 // status: the run's status read at kernel start (its load overlaps the tile's);
 // returns false -- after draining the bulk copy, before any global write --
 // when the run is no longer RUNNING (graph replays past the stop are no-ops)
-template <class T, int D, int KP1, int STAGE>
+// LATE (double scheme): the base operand is added in phase C (phase_c_store<LATE>)
+// instead of coming from shared memory here; acc holds s at stage 1, s/3 at
+// stage 4 and 0 otherwise, plus the increment
+template <class T, int D, int KP1, int STAGE, bool LATE = false>
 __device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, int own, T c,
                                         T (*sBase)[TILE], const uint8_t (*sN)[TILE],
                                         uint64_t* bar, T (&acc)[D * D],
@@ -162,6 +165,7 @@ __device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, in
         return (T)0;
       }
       if (STAGE == 1) return s[p];
+      if (LATE) return STAGE == 4 ? s[p] * third : (T)0;
       const T b = sBase[p][lane];
       if (STAGE == 2) sBase[p][lane] = (s[p] - b) * third;  // park (Y2 - s)/3 for B
       if (STAGE == 4) return fma(s[p], third, b);
@@ -255,16 +259,32 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
   }
 }
 
-template <class T, int D, int STAGE>
+template <class T, int D, int STAGE, bool LATE = false>
 __device__ __forceinline__ void phase_c_store(const KParams& P, int lane, int own,
                                               T (*sBase)[TILE], T (&acc)[D * D],
                                               double& maxa2, T (*sInc)[TILE] = nullptr) {
   constexpr int NP = D * D;
   constexpr T third = (T)(1.0 / 3.0), two3 = (T)(2.0 / 3.0);
+  if (LATE && STAGE >= 2) {  // base operands now: sigma (2, 3), B (4); stage 2 re-reads Y2
+    const T* bs = STAGE == 4 ? st_b<T>(P) : st_sig<T>(P);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const T sg = __ldg(bs + own + p * TILE);
+      if (STAGE == 2) {
+        const T y2 = __ldg(st_in<T>(P) + own + p * TILE);
+        acc[p] += sg;
+        st_b<T>(P)[own + p * TILE] = fma(two3, acc[p], (y2 - sg) * third);
+      } else {
+        acc[p] += sg;
+      }
+    }
+  }
   // ---- phase C: store (stage 2 also B = (Y2 - s)/3 + 2/3 Y3; float: see header)
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
-    if (kIncScheme<T>) {
+    if (LATE) {
+      st_out<T>(P)[own + p * TILE] = acc[p];
+    } else if (kIncScheme<T>) {
       const T a = acc[p], sg = sBase[p][lane];
       if (STAGE == 1) st_b<T>(P)[own + p * TILE] = a * third;
       if (STAGE == 2) st_b<T>(P)[own + p * TILE] = fma(two3, a, sInc[p][lane]);
