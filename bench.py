@@ -311,7 +311,8 @@ def run_b200(args):
         try:
             launches_ = json.loads(summ.read_text())["launches"]
             traffic = sum(e["dram_total_MB"] for e in launches_ if "k_" in e["kernel"]) * 1e6
-            kname = launches_[0]["kernel"]
+            kname = " | ".join(e["kernel"].split("(")[0].replace("void ", "")
+                               for e in launches_ if "k_" in e["kernel"])
         except (KeyError, ValueError, IndexError):
             traffic = None
 
@@ -370,7 +371,7 @@ def run_b200(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_unit": "DRAM bytes per RK4 step (4 stage launches), ncu",
                          "alg_bytes_per_step": B_ALG_STEP * n_tot,
-                         "kernel": f"{kname} .. stage 4 (4 launches per RK4 step; achieved = alg bytes / sum of stage times)",
+                         "kernel": f"{kname} (stages 1-4, one launch each per RK4 step; achieved = alg bytes / sum of stage times)",
                          "bytes_per_ado_step": B_ALG_STEP,
                          "stage_us": [round(1e3 * x, 2) for x in stage_ms],
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},

@@ -33,9 +33,10 @@ namespace hb {
 // VAR (experiments, HB_MM4_VAR): 1 = production; 5 = skip the neighbour crosses
 // (timing experiment for the streamed part alone; wrong results); 6 = production
 // with an idle second warp per CTA (half the resident working warps, same L1);
-// 7 = base operands read in phase C instead of bulk-copied to shared memory.
+// 7 = base operands read in phase C instead of bulk-copied to shared memory;
+// 8 = registers capped for 12 resident warps per SM (float path).
 template <class T, int D, int KP1, int STAGE, int VAR>
-__global__ void __launch_bounds__(VAR == 6 ? 64 : 32, 1) k_mm4(const KParams P) {
+__global__ void __launch_bounds__(VAR == 6 ? 64 : 32, VAR == 8 ? 12 : 1) k_mm4(const KParams P) {
   constexpr int NP = D * D;
   constexpr int M = D * KP1;
   constexpr int TB = NP * TILE;
@@ -128,7 +129,19 @@ static cudaError_t mm4_launch_b(int stage, const KParams& p, cudaStream_t s) {
 
 template <int D, int KP1>
 static cudaError_t mm4_launch_t(int stage, const KParams& p, cudaStream_t s) {
-  if (p.single) return mm4_launch_b<float, D, KP1, 1>(stage, p, s);
+  if (p.single) {
+    // float state: 168 registers (12 warps/SM) fit without spills; stages 1 and 3
+    // (10 KB of shared memory per CTA) gain from it, stages 2 and 4 (17 KB: L1 is
+    // squeezed to ~40 KB at 12 CTAs) do not.  HB_MM4_FVAR (experiments): 1 = never
+    // capped, 8 = capped at every stage, default = stages 1 and 3
+    static const int fvar = [] {
+      const char* e = getenv("HB_MM4_FVAR");
+      return e ? atoi(e) : 0;
+    }();
+    const bool cap = fvar == 8 || (fvar == 0 && (stage == 1 || stage == 3));
+    if (cap) return mm4_launch_b<float, D, KP1, 8>(stage, p, s);
+    return mm4_launch_b<float, D, KP1, 1>(stage, p, s);
+  }
   if constexpr (D == 7 && KP1 == 2) {
     static const int var = [] {
       const char* e = getenv("HB_MM4_VAR");
