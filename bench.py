@@ -223,6 +223,7 @@ def run_sharded(args, dist, world, rank, local):
     wall = time.perf_counter() - t0
     wall = allmax(dist, wall, f"cuda:{local}")
     halo = sr.plan.halo_tiles(rank)
+    halo_bytes = sr.cross_plan.bytes_per_stage(rank) if sr.cross_plan is not None else None
     launches = N_launch(sr.run_) - launches0
     sr.close()
     if rank == 0:
@@ -230,11 +231,11 @@ def run_sharded(args, dist, world, rank, local):
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {**config_dict(world), "parallelism": f"sharded x{world} (NCCL halo)",
-                           "halo_tiles_rank0": halo},
+                "config": {**config_dict(world),
+                           "parallelism": f"sharded x{world} (NCCL compressed cross halos)",
+                           "halo_tiles_rank0": halo,
+                           "halo_bytes_per_stage_rank0": halo_bytes},
                 "gpu_launches": int(launches),
-            "single_precision": single,
-            "eta_wall": eta or None,
                 "status": status}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -218,6 +218,20 @@ int hb_nccl_init(hb_handle* h, const char* id128, int nranks, int rank);
  * to / from rank peer[i] */
 int hb_exchange(hb_handle* h, int buf, int n, const int32_t* peer, const int32_t* first,
                 const int32_t* count, const int32_t* is_send);
+/* Compressed halos: a consumer reads from a halo ADO only the cross of the site
+ * it reaches it through (2d-1 Hermitian-packed planes, _kernels.py:41-57), so
+ * the plan lists (device position, site) entries instead of tiles.  Segment i
+ * has count[i] consecutive entries of pos/site, exchanged with rank peer[i]
+ * (is_send[i] = 1: this handle owns them).  Needs hb_set_rho0 first and the
+ * Hermitian production layout. */
+int hb_halo_set(hb_handle* h, int n_seg, const int32_t* peer, const int32_t* is_send,
+                const int32_t* count, const int32_t* pos, const int32_t* site);
+/* pack the send segments of buffer `buf`, grouped ncclSend/ncclRecv, unpack the
+ * receive segments -- all on the handle's stream */
+int hb_halo_exchange(hb_handle* h, int buf);
+/* in-process shards on one device: copy the crosses of receive segment `seg` of
+ * dst's plan from src's buffer `buf` into dst's, stream-ordered on both */
+int hb_halo_pull(hb_handle* dst, hb_handle* src, int buf, int seg);
 
 #ifdef __cplusplus
 }

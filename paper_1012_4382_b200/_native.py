@@ -29,7 +29,8 @@ EXPORTS = ("hb_last_error", "hb_device_count", "hb_hierarchy_size", "hb_graph_bu
            "hb_rhs", "hb_heom_rhs", "hb_add_scaled", "hb_rk4_update", "hb_max_abs2", "hb_create",
            "hb_destroy", "hb_set_rho0", "hb_run", "hb_get_records", "hb_record_count", "hb_get_state",
            "hb_get_sigma0", "hb_time_steps", "hb_launch_count", "hb_run_stage", "hb_sync",
-           "hb_copy_tiles", "hb_nccl_unique_id", "hb_nccl_init", "hb_exchange")
+           "hb_copy_tiles", "hb_nccl_unique_id", "hb_nccl_init", "hb_exchange",
+           "hb_halo_set", "hb_halo_exchange", "hb_halo_pull")
 
 
 class HbParams(C.Structure):
@@ -101,6 +102,9 @@ def lib():
         "hb_nccl_unique_id": (_i, [C.c_char_p]),
         "hb_nccl_init": (_i, [_p, C.c_char_p, _i, _i]),
         "hb_exchange": (_i, [_p, _i, _i, _p, _p, _p, _p]),
+        "hb_halo_set": (_i, [_p, _i, _p, _p, _p, _p, _p]),
+        "hb_halo_exchange": (_i, [_p, _i]),
+        "hb_halo_pull": (_i, [_p, _p, _i, _i]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -7,6 +7,7 @@
 // graph and synchronises once per chunk to drain records and read the status
 // written by the last CTA of each stage-4 kernel (hb_stage.cu).
 #include <dlfcn.h>
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -112,7 +113,24 @@ struct hb_handle {
   bool ready = false;  // rho0 set
   int own_begin = 0, own_count = 0;  // sharding: owned tile range
   void* nccl_comm = nullptr;
+  // compressed halo plan (hb_halo_set): segments of (position, site) entries
+  struct Halo {
+    int nc = 0;                                    // planes per cross (2d - 1)
+    std::vector<int> peer, is_send, count, off;    // per segment; off in entries
+    int32_t* pos = nullptr;                        // device, all segments
+    int32_t* site = nullptr;
+    int16_t* planes = nullptr;                     // device, [site][nc] plane index
+    void* packed = nullptr;                        // device staging, [entry][nc]
+  } halo;
 };
+
+static void free_halo(hb_handle* h) {
+  cudaFree(h->halo.pos);
+  cudaFree(h->halo.site);
+  cudaFree(h->halo.planes);
+  cudaFree(h->halo.packed);
+  h->halo = hb_handle::Halo{};
+}
 
 // definitions take C linkage from the extern "C" declarations in heom_b200.h
 
@@ -343,6 +361,7 @@ void hb_destroy(hb_handle* h) {
   if (h->nccl_comm) nccl_destroy(h->nccl_comm);
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_state(h);
+  free_halo(h);
   h->graph_ref.reset();
   cudaFree(h->ctl);
   cudaFreeHost(h->ctl_host);
@@ -998,3 +1017,119 @@ int hb_exchange(hb_handle* h, int buf, int n, const int32_t* peer, const int32_t
   r = nccl().group_end();
   return r ? nccl_fail(r, "ncclGroupEnd") : HB_OK;
 }
+
+// ---- compressed halos (hb_halo.cu) ----
+
+int hb_halo_set(hb_handle* h, int n_seg, const int32_t* peer, const int32_t* is_send,
+                const int32_t* count, const int32_t* pos, const int32_t* site) {
+  if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
+  if (!h->base.fast || h->layout != HB_LAYOUT_HERMITIAN)
+    return fail(HB_ERR_ARG, "compressed halos need the Hermitian production layout");
+  if (n_seg < 0) return fail(HB_ERR_ARG, "negative segment count");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->stream));
+  free_halo(h);
+  const int d = h->prm.d, nc = 2 * d - 1;
+  auto& H = h->halo;
+  H.nc = nc;
+  int64_t total = 0;
+  for (int i = 0; i < n_seg; ++i) {
+    if (count[i] < 0) return fail(HB_ERR_ARG, "negative segment size");
+    H.peer.push_back(peer[i]);
+    H.is_send.push_back(is_send[i] != 0);
+    H.count.push_back(count[i]);
+    H.off.push_back((int)total);
+    total += count[i];
+  }
+  if (total > INT32_MAX / nc) return fail(HB_ERR_ARG, "halo plan too large");
+  for (int64_t e = 0; e < total; ++e) {
+    if (pos[e] < 0 || pos[e] >= h->n_tot) return fail(HB_ERR_ARG, "halo position outside the hierarchy");
+    if (site[e] < 0 || site[e] >= d) return fail(HB_ERR_ARG, "halo site outside the block");
+  }
+  // Hermitian-packed planes of the cross of block position s (row/column s)
+  std::vector<int16_t> planes((size_t)d * nc);
+  auto packed_off = [&](int a, int b) {  // a < b
+    int e = 0;
+    for (int r = 0; r < a; ++r) e += d - 1 - r;
+    return e + (b - a - 1);
+  };
+  for (int s = 0; s < d; ++s) {
+    int q = 0;
+    planes[(size_t)s * nc + q++] = (int16_t)s;
+    for (int o = 0; o < d; ++o) {
+      if (o == s) continue;
+      const int re = d + 2 * packed_off(s < o ? s : o, s < o ? o : s);
+      planes[(size_t)s * nc + q++] = (int16_t)re;
+      planes[(size_t)s * nc + q++] = (int16_t)(re + 1);
+    }
+  }
+  const size_t ib = (size_t)std::max<int64_t>(total, 1) * sizeof(int32_t);
+  CK(cudaMalloc(&H.pos, ib));
+  CK(cudaMalloc(&H.site, ib));
+  CK(cudaMalloc(&H.planes, planes.size() * sizeof(int16_t)));
+  CK(cudaMalloc(&H.packed, (size_t)std::max<int64_t>(total, 1) * nc * elem_size(h)));
+  if (total) {
+    CK(cudaMemcpy(H.pos, pos, total * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(H.site, site, total * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemcpy(H.planes, planes.data(), planes.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+  return HB_OK;
+}
+
+int hb_halo_exchange(hb_handle* h, int buf) {
+  if (!h || !h->ready || !h->nccl_comm) return fail(HB_ERR_ARG, "handle without NCCL communicator");
+  if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
+  CK(cudaSetDevice(h->device));
+  auto& H = h->halo;
+  const bool single = h->base.single;
+  const size_t eb = elem_size(h);
+  auto seg_ptr = [&](int i) { return static_cast<char*>(H.packed) + (size_t)H.off[i] * H.nc * eb; };
+  for (size_t i = 0; i < H.count.size(); ++i)  // pack every send segment
+    if (H.is_send[i])
+      CK(launch_halo(0, single, nullptr, h->buf[buf], H.count[i], H.pos + H.off[i],
+                     H.site + H.off[i], H.planes, H.nc, h->n_planes, seg_ptr((int)i), h->stream));
+  int r = nccl().group_start();
+  if (r) return nccl_fail(r, "ncclGroupStart");
+  for (size_t i = 0; i < H.count.size(); ++i) {
+    const size_t bytes = (size_t)H.count[i] * H.nc * eb;
+    r = H.is_send[i] ? nccl().send(seg_ptr((int)i), bytes, 0, H.peer[i], h->nccl_comm, h->stream)
+                     : nccl().recv(seg_ptr((int)i), bytes, 0, H.peer[i], h->nccl_comm, h->stream);
+    if (r) {
+      nccl().group_end();
+      return nccl_fail(r, H.is_send[i] ? "ncclSend" : "ncclRecv");
+    }
+  }
+  r = nccl().group_end();
+  if (r) return nccl_fail(r, "ncclGroupEnd");
+  for (size_t i = 0; i < H.count.size(); ++i)  // scatter every receive segment
+    if (!H.is_send[i])
+      CK(launch_halo(1, single, h->buf[buf], nullptr, H.count[i], H.pos + H.off[i],
+                     H.site + H.off[i], H.planes, H.nc, h->n_planes, seg_ptr((int)i), h->stream));
+  return HB_OK;
+}
+
+int hb_halo_pull(hb_handle* dst, hb_handle* src, int buf, int seg) {
+  if (!dst || !src || !dst->ready || !src->ready) return fail(HB_ERR_ARG, "handles not ready");
+  if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
+  if (dst->device != src->device) return fail(HB_ERR_ARG, "hb_halo_pull needs both shards on one device");
+  if (dst->n_planes != src->n_planes || dst->n_tiles != src->n_tiles ||
+      dst->base.single != src->base.single)
+    return fail(HB_ERR_ARG, "handles have different layouts");
+  auto& H = dst->halo;
+  if (seg < 0 || seg >= (int)H.count.size() || H.is_send[seg])
+    return fail(HB_ERR_ARG, "not a receive segment of the destination's halo plan");
+  CK(cudaSetDevice(dst->device));
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, src->stream));
+  CK(cudaStreamWaitEvent(dst->stream, ev, 0));
+  CK(launch_halo(2, dst->base.single, dst->buf[buf], src->buf[buf], H.count[seg],
+                 H.pos + H.off[seg], H.site + H.off[seg], H.planes, H.nc, dst->n_planes, nullptr,
+                 dst->stream));
+  // the source must not overwrite the crosses before the copy has read them
+  CK(cudaEventRecord(ev, dst->stream));
+  CK(cudaStreamWaitEvent(src->stream, ev, 0));
+  CK(cudaEventDestroy(ev));
+  return HB_OK;
+}
+

@@ -1,0 +1,76 @@
+// Compressed halo exchange for sharded propagation.
+//
+// A shard's stage kernel reads, from a neighbour ADO reached through mode m,
+// only the cross of site(m): the 2d-1 Hermitian-packed planes of row/column
+// site(m) (_kernels.py:41-57 reads element (i,j) of a neighbour only when i or
+// j is that mode's site).  So instead of whole tiles (32 ADOs x d^2 planes) a
+// consumer needs, per halo ADO, just the crosses of the sites it reaches it
+// through: entries (device position t, site s), 13 doubles each at d = 7.
+// At N_max = 8, K = 1 that cuts the halo ~3.7x (62.5 -> 17 MB per
+// stage per GPU at P = 8).
+//   pack   : owner, entries of one send segment -> contiguous [entry][plane]
+//   unpack : consumer, contiguous -> the same planes of its full-size buffer
+//   copy   : in-process shards on one device, owner buffer -> consumer buffer
+#include "hb_internal.h"
+
+namespace hb {
+
+template <class T>
+__global__ void k_halo_pack(const T* __restrict__ buf, int n, const int32_t* __restrict__ pos,
+                            const int32_t* __restrict__ site, const int16_t* __restrict__ planes,
+                            int nc, int n_planes, T* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * nc) return;
+  const int e = (int)(idx / nc), q = (int)(idx % nc);
+  const int t = pos[e];
+  const int p = planes[site[e] * nc + q];
+  out[idx] = buf[(size_t)(t >> 5) * n_planes * TILE + (size_t)p * TILE + (t & 31)];
+}
+
+template <class T>
+__global__ void k_halo_unpack(T* __restrict__ buf, int n, const int32_t* __restrict__ pos,
+                              const int32_t* __restrict__ site, const int16_t* __restrict__ planes,
+                              int nc, int n_planes, const T* __restrict__ in) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * nc) return;
+  const int e = (int)(idx / nc), q = (int)(idx % nc);
+  const int t = pos[e];
+  const int p = planes[site[e] * nc + q];
+  buf[(size_t)(t >> 5) * n_planes * TILE + (size_t)p * TILE + (t & 31)] = in[idx];
+}
+
+template <class T>
+__global__ void k_halo_copy(T* __restrict__ dst, const T* __restrict__ src, int n,
+                            const int32_t* __restrict__ pos, const int32_t* __restrict__ site,
+                            const int16_t* __restrict__ planes, int nc, int n_planes) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * nc) return;
+  const int e = (int)(idx / nc), q = (int)(idx % nc);
+  const int t = pos[e];
+  const int p = planes[site[e] * nc + q];
+  const size_t a = (size_t)(t >> 5) * n_planes * TILE + (size_t)p * TILE + (t & 31);
+  dst[a] = src[a];
+}
+
+static unsigned blocks(int n, int nc) { return (unsigned)(((int64_t)n * nc + 255) / 256); }
+
+cudaError_t launch_halo(int op, bool single, void* dst, const void* src, int n, const int32_t* pos,
+                        const int32_t* site, const int16_t* planes, int nc, int n_planes,
+                        void* packed, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned g = blocks(n, nc);
+  if (single) {
+    using T = float;
+    if (op == 0) k_halo_pack<T><<<g, 256, 0, s>>>((const T*)src, n, pos, site, planes, nc, n_planes, (T*)packed);
+    if (op == 1) k_halo_unpack<T><<<g, 256, 0, s>>>((T*)dst, n, pos, site, planes, nc, n_planes, (const T*)packed);
+    if (op == 2) k_halo_copy<T><<<g, 256, 0, s>>>((T*)dst, (const T*)src, n, pos, site, planes, nc, n_planes);
+  } else {
+    using T = double;
+    if (op == 0) k_halo_pack<T><<<g, 256, 0, s>>>((const T*)src, n, pos, site, planes, nc, n_planes, (T*)packed);
+    if (op == 1) k_halo_unpack<T><<<g, 256, 0, s>>>((T*)dst, n, pos, site, planes, nc, n_planes, (const T*)packed);
+    if (op == 2) k_halo_copy<T><<<g, 256, 0, s>>>((T*)dst, (const T*)src, n, pos, site, planes, nc, n_planes);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hb

@@ -123,6 +123,12 @@ cudaError_t launch_elementwise(int op, int64_t n, double* out, const double* x,
 cudaError_t launch_max_abs2(int64_t n, const double* x, unsigned long long* bits,
                             cudaStream_t s);
 
+// hb_halo.cu: compressed (cross-only) halo exchange; op 0 = pack src -> packed,
+// 1 = unpack packed -> dst, 2 = copy src -> dst (same addresses)
+cudaError_t launch_halo(int op, bool single, void* dst, const void* src, int n, const int32_t* pos,
+                        const int32_t* site, const int16_t* planes, int nc, int n_planes,
+                        void* packed, cudaStream_t s);
+
 // hb_graph.cu
 struct GraphTables {
   int modes, n_max, n_tot, n_tiles;

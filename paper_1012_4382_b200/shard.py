@@ -19,6 +19,12 @@ After stage s every owner sends those runs of the stage-s output buffer
 * ``NcclShardedRun``  -- one process per GPU (torchrun); grouped
   ncclSend/ncclRecv of the same tile runs (hb_exchange), NCCL over NVLink.
 
+Both default to COMPRESSED halos (``exchange='crosses'``, cross_halo_plan): a
+consumer reads from a halo ADO only the cross of the site it reaches it
+through, so the plan ships (position, site) entries of 2d-1 planes instead of
+whole tiles -- packed, grouped ncclSend/ncclRecv, unpacked (hb_halo_exchange),
+or, for in-process shards on one device, copied in place (hb_halo_pull).
+
 The root shard (tile 0 = ADO 0) integrates the sinks and records; sharded runs
 use the t_end policy (a fixed number of steps, e.g. config 4: 1 ps).
 """
@@ -105,6 +111,65 @@ def halo_plan(plus_dev: np.ndarray, minus_dev: np.ndarray, n_shards: int) -> Hal
     return HaloPlan(ranges=ranges, recv=recv, send=send)
 
 
+@dataclass
+class CrossHaloPlan:
+    """Compressed halos: per (consumer, owner) the (device position, site)
+    entries whose cross (2d-1 planes) the consumer's kernels read."""
+    ranges: list          # [(begin, count)] per shard
+    recv: list            # recv[q] = [(owner, pos int32[], site int32[])]
+    send: list            # send[o] = [(consumer, pos, site)] (the same arrays)
+    n_planes_cross: int   # 2d - 1
+
+    def entries(self, q: int) -> int:
+        return sum(len(p) for _, p, _ in self.recv[q])
+
+    def bytes_per_stage(self, q: int, elem: int = 8) -> int:
+        return self.entries(q) * self.n_planes_cross * elem
+
+
+def cross_halo_plan(plus_dev: np.ndarray, minus_dev: np.ndarray, n_shards: int, kp1: int,
+                    d: int) -> CrossHaloPlan:
+    """Mode m of the tables belongs to site m // kp1 (slot s = j(K+1) + k,
+    identity site_of); a consumer reaching ADO t through mode m reads only the
+    cross of that site (_kernels.py:41-57)."""
+    n_tot, modes = plus_dev.shape
+    n_tiles = (n_tot + TILE - 1) // TILE
+    ranges = shard_ranges(n_tiles, n_shards)
+    owner_of_tile = np.empty(n_tiles, np.int64)
+    for r, (b, c) in enumerate(ranges):
+        owner_of_tile[b:b + c] = r
+    site_of_mode = np.arange(modes) // kp1
+    recv = [[] for _ in range(n_shards)]
+    send = [[] for _ in range(n_shards)]
+    for q, (b, c) in enumerate(ranges):
+        lo, hi = b * TILE, min((b + c) * TILE, n_tot)
+        t = np.concatenate([plus_dev[lo:hi], minus_dev[lo:hi]]).astype(np.int64)
+        s = np.broadcast_to(site_of_mode, t.shape)
+        keep = (t >= 0) & ((t < b * TILE) | (t >= (b + c) * TILE))
+        key = np.unique(t[keep] * 16 + s[keep])          # sorted by position, then site
+        tt, ss = key // 16, key % 16
+        own = owner_of_tile[tt // TILE]
+        for owner in np.unique(own):
+            sel = own == owner
+            pos = np.ascontiguousarray(tt[sel], np.int32)
+            site = np.ascontiguousarray(ss[sel], np.int32)
+            recv[q].append((int(owner), pos, site))
+            send[int(owner)].append((q, pos, site))
+    return CrossHaloPlan(ranges=ranges, recv=recv, send=send, n_planes_cross=2 * d - 1)
+
+
+def _halo_set(run: DeviceRun, segments):
+    """segments: [(peer, is_send, pos, site)] -> hb_halo_set"""
+    i32 = lambda x: np.ascontiguousarray(x, np.int32)
+    peer = i32([g[0] for g in segments] or [0])
+    is_send = i32([g[1] for g in segments] or [0])
+    count = i32([len(g[2]) for g in segments] or [0])
+    pos = i32(np.concatenate([g[2] for g in segments]) if segments else [0])
+    site = i32(np.concatenate([g[3] for g in segments]) if segments else [0])
+    N.check(N.lib().hb_halo_set(run._h, len(segments), N.ptr(peer), N.ptr(is_send), N.ptr(count),
+                                N.ptr(pos), N.ptr(site)), "hb_halo_set")
+
+
 def stage_output_buffer(stage: int) -> int:
     """Buffer index written by a stage: 1 -> Y2 (1), 2 -> Y3 (2), 3 -> Y4 (3), 4 -> sigma (0)."""
     return stage % 4
@@ -115,22 +180,40 @@ class ShardedRun:
 
     def __init__(self, ops: BlockOperands, n_max: int, dt_fs: float, t_end_fs: float,
                  n_shards: int, devices=None, record_stride: int = 1,
-                 record_matrices: bool = False, blowup_norm: float = 1e6):
+                 record_matrices: bool = False, blowup_norm: float = 1e6,
+                 exchange: str = "crosses", precision: str = "double"):
         devices = devices or [0] * n_shards
+        if exchange not in ("crosses", "tiles"):
+            raise ValueError("exchange must be 'crosses' or 'tiles'")
+        if exchange == "crosses" and len(set(devices)) > 1:
+            raise ValueError("in-process compressed halos need all shards on one device")
         pd, md = device_order_tables(ops.modes, n_max, devices[0])
+        self.exchange = exchange
         self.plan = halo_plan(pd, md, n_shards)
+        self.cross_plan = cross_halo_plan(pd, md, n_shards, ops.n_matsubara + 1, ops.d) \
+            if exchange == "crosses" else None
         self.n_tot = pd.shape[0]
         self.runs = [DeviceRun(ops, n_max, dt_fs, t_end_fs=t_end_fs, record_stride=record_stride,
                                record_matrices=record_matrices, blowup_norm=blowup_norm,
-                               device=devices[q], layout="hermitian", tile_range=rg)
+                               device=devices[q], layout="hermitian", tile_range=rg,
+                               precision=precision)
                      for q, rg in enumerate(self.plan.ranges)]
 
     def set_rho0(self, rho0_block, sink_pops):
         for r in self.runs:
             r.set_rho0(rho0_block, sink_pops)
+        if self.cross_plan is not None:
+            for q, r in enumerate(self.runs):
+                _halo_set(r, [(o, 0, p, s) for o, p, s in self.cross_plan.recv[q]])
 
     def _exchange(self, stage: int):
         buf = stage_output_buffer(stage)
+        if self.cross_plan is not None:
+            for q, recv in enumerate(self.cross_plan.recv):
+                for seg, (owner, _, _) in enumerate(recv):
+                    N.check(N.lib().hb_halo_pull(self.runs[q]._h, self.runs[owner]._h, buf, seg),
+                            "hb_halo_pull")
+            return
         for q, recv in enumerate(self.plan.recv):
             for owner, first, cnt in recv:
                 N.check(N.lib().hb_copy_tiles(self.runs[q]._h, self.runs[owner]._h, buf, first, cnt),
@@ -169,9 +252,12 @@ class NcclShardedRun:
     """One process per GPU (torch.distributed initialised); NCCL halo exchange."""
 
     def __init__(self, ops: BlockOperands, n_max: int, dt_fs: float, t_end_fs: float,
-                 rank: int, world: int, device: int, dist, record_stride: int = 10 ** 9):
+                 rank: int, world: int, device: int, dist, record_stride: int = 10 ** 9,
+                 exchange: str = "crosses"):
         pd, md = device_order_tables(ops.modes, n_max, device)
         self.plan = halo_plan(pd, md, world)
+        self.cross_plan = cross_halo_plan(pd, md, world, ops.n_matsubara + 1, ops.d) \
+            if exchange == "crosses" else None
         self.rank, self.world = rank, world
         self.run_ = DeviceRun(ops, n_max, dt_fs, t_end_fs=t_end_fs, record_stride=record_stride,
                               device=device, layout="hermitian", tile_range=self.plan.ranges[rank])
@@ -189,13 +275,21 @@ class NcclShardedRun:
 
     def set_rho0(self, rho0_block, sink_pops):
         self.run_.set_rho0(rho0_block, sink_pops)
+        if self.cross_plan is not None:
+            cp, r = self.cross_plan, self.rank
+            _halo_set(self.run_, [(o, 0, p, s) for o, p, s in cp.recv[r]] +
+                                 [(c, 1, p, s) for c, p, s in cp.send[r]])
 
     def enqueue_step(self):
         L = N.lib()
         for s in (1, 2, 3, 4):
             N.check(L.hb_run_stage(self.run_._h, s), "hb_run_stage")
-            N.check(L.hb_exchange(self.run_._h, stage_output_buffer(s), self._n_ex,
-                                  *(N.ptr(a) for a in self._ex)), "hb_exchange")
+            if self.cross_plan is not None:
+                N.check(L.hb_halo_exchange(self.run_._h, stage_output_buffer(s)),
+                        "hb_halo_exchange")
+            else:
+                N.check(L.hb_exchange(self.run_._h, stage_output_buffer(s), self._n_ex,
+                                      *(N.ptr(a) for a in self._ex)), "hb_exchange")
 
     def sync(self):
         st, step = C.c_int(0), C.c_int64(0)

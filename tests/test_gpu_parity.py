@@ -263,8 +263,9 @@ def test_dense_rk4_matches_reference_and_fast_path():
 
 # ------------------------------------------------- sharding (8(e)), one GPU
 
+@pytest.mark.parametrize("exchange", ["crosses", "tiles"])
 @pytest.mark.parametrize("n_shards,n_max", [(2, 3), (3, 3), (4, 5)])
-def test_sharded_run_is_bit_exact(n_shards, n_max):
+def test_sharded_run_is_bit_exact(n_shards, n_max, exchange):
     from paper_1012_4382_b200.shard import ShardedRun
     ops = BlockOperands(FMO, BATH300, RATES, 1)
     rho0 = np.zeros((7, 7), complex)
@@ -274,7 +275,7 @@ def test_sharded_run_is_bit_exact(n_shards, n_max):
         assert ref.run() == N.HB_OK
         steps_ref, pops_ref, _ = ref.records()
         sig_ref, sinks_ref = ref.sigma0()
-    sr = ShardedRun(ops, n_max, 1.0, 30.0, n_shards)
+    sr = ShardedRun(ops, n_max, 1.0, 30.0, n_shards, exchange=exchange)
     try:
         assert sum(sr.plan.halo_tiles(q) for q in range(n_shards)) > 0
         sr.set_rho0(rho0, [0.0, 0.0])
@@ -286,6 +287,25 @@ def test_sharded_run_is_bit_exact(n_shards, n_max):
     assert np.array_equal(steps, steps_ref)
     assert np.array_equal(pops, pops_ref)          # bit-exact: same kernels, complete halos
     assert np.array_equal(sig, sig_ref) and np.array_equal(sinks, sinks_ref)
+
+
+def test_sharded_single_precision_is_bit_exact():
+    from paper_1012_4382_b200.shard import ShardedRun
+    ops = BlockOperands(FMO, BATH300, RATES, 1)
+    rho0 = np.zeros((7, 7), complex)
+    rho0[0, 0] = 1.0
+    with DeviceRun(ops, 3, 1.0, t_end_fs=30.0, layout="hermitian", precision="single") as ref:
+        ref.set_rho0(rho0, [0.0, 0.0])
+        assert ref.run() == N.HB_OK
+        _, pops_ref, _ = ref.records()
+    sr = ShardedRun(ops, 3, 1.0, 30.0, 3, precision="single")
+    try:
+        sr.set_rho0(rho0, [0.0, 0.0])
+        assert sr.run() == 1
+        _, pops, _ = sr.records()
+    finally:
+        sr.close()
+    assert np.array_equal(pops, pops_ref)
 
 
 # ------------------------------------------------- sweeps (8(f) rank 2)

@@ -8,8 +8,8 @@ import numpy as np
 import pytest
 
 from oracle import oracle as orc
-from paper_1012_4382_b200.shard import (TILE, device_tables_from_reference, halo_plan,
-                                        shard_ranges, stage_output_buffer)
+from paper_1012_4382_b200.shard import (TILE, cross_halo_plan, device_tables_from_reference,
+                                        halo_plan, shard_ranges, stage_output_buffer)
 
 
 def lex_perm(indices):
@@ -52,6 +52,30 @@ def test_halo_plan_is_complete_and_minimal(modes, n_max, shards):
         assert all(0 <= t < n_tiles for t in halo)
     sends = sorted((o, q, f, c) for q in range(shards) for o, f, c in plan.recv[q])
     assert sends == sorted((o, q, f, c) for o in range(shards) for q, f, c in plan.send[o])
+
+
+@pytest.mark.parametrize("modes,kp1,n_max,shards", [(14, 2, 3, 2), (14, 2, 4, 5), (7, 1, 6, 3)])
+def test_cross_halo_plan_is_complete_and_minimal(modes, kp1, n_max, shards):
+    ind, _, plus, minus = orc.enumerate_hierarchy(modes, n_max)
+    perm = lex_perm(ind)
+    pd, md = device_tables_from_reference(plus, minus, perm)
+    plan = cross_halo_plan(pd, md, shards, kp1, 7)
+    for q, (b, c) in enumerate(plan.ranges):
+        lo, hi = b * TILE, min((b + c) * TILE, len(ind))
+        need = set()
+        for m in range(modes):
+            for t in np.concatenate([pd[lo:hi, m], md[lo:hi, m]]):
+                if t >= 0 and not (b * TILE <= t < (b + c) * TILE):
+                    need.add((int(t), m // kp1))
+        got = set()
+        for owner, pos, site in plan.recv[q]:
+            ob, oc = plan.ranges[owner]
+            assert np.all((pos >= ob * TILE) & (pos < (ob + oc) * TILE))
+            assert np.all(np.diff(pos.astype(np.int64) * 16 + site) > 0)   # sorted, unique
+            got |= set(zip(pos.tolist(), site.tolist()))
+        assert got == need                      # complete and minimal
+    pairs = sorted((o, q, len(p)) for q in range(shards) for o, p, _ in plan.recv[q])
+    assert pairs == sorted((o, q, len(p)) for o in range(shards) for q, p, _ in plan.send[o])
 
 
 def test_stage_buffers():
@@ -104,6 +128,71 @@ def _worker(rank, world, port, out_q):
     ok = np.array_equal(rhs_local[mine], rhs_full[mine])
     out_q.put((rank, ok, len(mine), plan.halo_tiles(rank)))
     dist.destroy_process_group()
+
+
+def _cross_worker(rank, world, port, out_q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1012_4382_b200 as xf
+    fmo = xf.build_fmo_system()
+    bath = xf.BathParams.from_timescale(35.0, 166.0, 300.0)
+    rates = xf.MarkovRates.from_inverse_ps(2.5, 250.0)
+    pb = orc.Problem(fmo, bath, rates, 3, 1)
+    perm = lex_perm(pb.indices)
+    pd, md = device_tables_from_reference(pb.plus, pb.minus, perm)
+    plan = cross_halo_plan(pd, md, world, 2, 7)
+    rng = np.random.default_rng(12)
+    full = rng.standard_normal((pb.n_tot, 7, 7)) + 1j * rng.standard_normal((pb.n_tot, 7, 7))
+    full = full + full.conj().transpose(0, 2, 1)          # Hermitian, like every ADO
+    n_pad = ((pb.n_tot + TILE - 1) // TILE) * TILE
+    dev = np.zeros((n_pad, 7, 7), complex)
+    dev[perm] = full
+    b, c = plan.ranges[rank]
+    local = np.full_like(dev, np.nan)      # everything this rank does not own: unknown
+    local[b * TILE:(b + c) * TILE] = dev[b * TILE:(b + c) * TILE]
+
+    def cross(m, s):  # row and column s of each matrix: the 2d-1 shipped elements
+        return np.concatenate([m[:, s, :], m[:, :, s]], axis=1)
+
+    reqs = []
+    for dst, pos, site in plan.send[rank]:
+        payload = np.stack([cross(local[pos[i]:pos[i] + 1], site[i])[0] for i in range(len(pos))])
+        reqs.append(dist.isend(torch.from_numpy(payload.view(np.float64).copy()), dst))
+    for owner, pos, site in plan.recv[rank]:
+        t = torch.empty((len(pos), 14, 2), dtype=torch.float64)
+        dist.recv(t, owner)
+        got = t.numpy().view(np.complex128)[..., 0]
+        for i in range(len(pos)):
+            local[pos[i], site[i], :] = got[i, :7]
+            local[pos[i], :, site[i]] = got[i, 7:]
+    for r in reqs:
+        r.wait()
+    rhs_local = pb.rhs(local[perm])
+    rhs_full = pb.rhs(full)
+    mine = [k for k in range(pb.n_tot) if b * TILE <= perm[k] < (b + c) * TILE]
+    ok = np.array_equal(rhs_local[mine], rhs_full[mine])
+    out_q.put((rank, ok, len(mine), plan.entries(rank)))
+    dist.destroy_process_group()
+
+
+def test_gloo_cross_halo_exchange_reproduces_unsharded_rhs():
+    """only the crosses are shipped; the rest of every halo ADO is NaN here, so
+    a kernel reading any other element of a neighbour would fail"""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cross_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[1] for r in res] == [True, True]
+    assert sum(r[2] for r in res) == orc.hierarchy_size(14, 3)
+    assert all(r[3] > 0 for r in res)
 
 
 def test_gloo_halo_exchange_reproduces_unsharded_rhs():
