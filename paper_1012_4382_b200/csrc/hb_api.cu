@@ -97,6 +97,7 @@ struct hb_handle {
   int layout = 0;  // HB_LAYOUT_HERMITIAN / GENERAL once allocated
   int n_planes = 0;
   double* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // sigma, Y2, Y3, Y4, B
+  size_t buf_bytes = 0;
   double* zero_tile = nullptr;  // never written: target of absent links
   Ctl* ctl = nullptr;
   Ctl* ctl_host = nullptr;  // pinned
@@ -107,6 +108,7 @@ struct hb_handle {
   KParams base{};
   cudaGraphExec_t graph = nullptr;
   int graph_layout = -1;
+  std::string graph_key;  // GraphCache key of `graph`
   std::vector<int64_t> steps;
   std::vector<double> pops, mats;
   int64_t launches = 0;
@@ -343,13 +345,96 @@ int hb_max_abs2(const double* x, int64_t n, double* result, int device) {
 // ---------------------------------------------------------------------------
 // Level-1 propagator
 
+// Device buffer pool: propagate() creates and destroys a handle per call, and
+// cudaMalloc/cudaFree of the 4-5 state buffers (125 MB each at config 4) is
+// synchronous and costs milliseconds; released buffers are kept per (device,
+// size) up to kPoolCap bytes and handed to the next handle of the same shape
+// (which zeroes them, alloc_state).
+struct BufPool {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> idle;
+  size_t cached = 0;
+};
+static BufPool& buf_pool() {
+  static BufPool* p = new BufPool();  // never destroyed: the driver reclaims at exit
+  return *p;
+}
+constexpr size_t kPoolCap = size_t(24) << 30;
+
+static cudaError_t pool_alloc(int device, size_t bytes, void** out) {
+  {
+    BufPool& P = buf_pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = P.idle.find({device, bytes});
+    if (it != P.idle.end()) {
+      *out = it->second;
+      P.idle.erase(it);
+      P.cached -= bytes;
+      return cudaSuccess;
+    }
+  }
+  return cudaMalloc(out, bytes);
+}
+
+static void pool_release(int device, size_t bytes, void* p) {
+  BufPool& P = buf_pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  if (P.cached + bytes > kPoolCap) {
+    cudaFree(p);
+    return;
+  }
+  P.idle.insert({{device, bytes}, p});
+  P.cached += bytes;
+}
+
+// Instantiated step graphs, keyed by the bytes of the four stages' kernel
+// parameters (+ chunk and device): instantiating 4 x chunk_steps kernel nodes
+// costs ~20 ms at chunk 64, as much as a few hundred steps of a small
+// hierarchy.  With pooled buffers a repeated propagate() of the same shape sees
+// identical parameters and replays the cached graph.  A graph is owned by at
+// most one handle at a time (identical parameters mean identical buffers, which
+// the pool never hands to two live handles).
+struct GraphCache {
+  std::mutex mu;
+  std::vector<std::pair<std::string, cudaGraphExec_t>> lru;  // most recent last
+};
+static GraphCache& graph_cache() {
+  static GraphCache* c = new GraphCache();
+  return *c;
+}
+constexpr size_t kGraphCacheCap = 8;
+
+static void graph_cache_put(hb_handle* h) {
+  if (!h->graph) return;
+  GraphCache& G = graph_cache();
+  std::lock_guard<std::mutex> lk(G.mu);
+  G.lru.emplace_back(h->graph_key, h->graph);
+  if (G.lru.size() > kGraphCacheCap) {
+    cudaGraphExecDestroy(G.lru.front().second);
+    G.lru.erase(G.lru.begin());
+  }
+  h->graph = nullptr;
+}
+
+static cudaGraphExec_t graph_cache_take(const std::string& key) {
+  GraphCache& G = graph_cache();
+  std::lock_guard<std::mutex> lk(G.mu);
+  for (auto it = G.lru.rbegin(); it != G.lru.rend(); ++it)
+    if (it->first == key) {
+      cudaGraphExec_t g = it->second;
+      G.lru.erase(std::next(it).base());
+      return g;
+    }
+  return nullptr;
+}
+
 static void free_state(hb_handle* h) {
+  if (h->stream) cudaStreamSynchronize(h->stream);  // no work in flight on the buffers
   for (auto& b : h->buf) {
-    if (b) cudaFree(b);
+    if (b) pool_release(h->device, h->buf_bytes, b);
     b = nullptr;
   }
-  if (h->graph) cudaGraphExecDestroy(h->graph);
-  h->graph = nullptr;
+  graph_cache_put(h);
   h->graph_layout = -1;
 }
 
@@ -363,11 +448,15 @@ void hb_destroy(hb_handle* h) {
   free_state(h);
   free_halo(h);
   h->graph_ref.reset();
-  cudaFree(h->ctl);
+  const size_t zbytes = (size_t)2 * MAXD * MAXD * TILE * sizeof(double);
+  if (h->ctl) pool_release(h->device, sizeof(Ctl), h->ctl);
+  if (h->zero_tile) pool_release(h->device, zbytes, h->zero_tile);
   cudaFreeHost(h->ctl_host);
-  cudaFree(h->rec_step);
-  cudaFree(h->rec_pops);
-  cudaFree(h->rec_mats);
+  if (h->rec_step) pool_release(h->device, h->rec_cap * sizeof(long long), h->rec_step);
+  if (h->rec_pops) pool_release(h->device, h->rec_cap * h->prm.d_full * sizeof(double), h->rec_pops);
+  if (h->rec_mats)
+    pool_release(h->device, h->rec_cap * h->prm.d_full * h->prm.d_full * 2 * sizeof(double),
+                 h->rec_mats);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -442,19 +531,25 @@ int hb_create(const hb_params* P, hb_handle** out) {
     hb_destroy(h);
     return fail(HB_ERR_ARG, "sharded runs need the t_end stop policy");
   }
-  e = cudaMalloc(&h->ctl, sizeof(Ctl));
+  // small per-handle buffers come from the pool too: a handle of the same shape
+  // then gets the same pointers, hence byte-identical kernel parameters, and can
+  // reuse a cached instantiated CUDA graph (ensure_graph)
+  e = pool_alloc(h->device, sizeof(Ctl), reinterpret_cast<void**>(&h->ctl));
   if (e) return bail(e, "cudaMalloc(ctl)");
   const size_t zbytes = (size_t)2 * MAXD * MAXD * TILE * sizeof(double);
-  e = cudaMalloc(&h->zero_tile, zbytes);
+  e = pool_alloc(h->device, zbytes, reinterpret_cast<void**>(&h->zero_tile));
   if (!e) e = cudaMemsetAsync(h->zero_tile, 0, zbytes, h->stream);
   if (e) return bail(e, "cudaMalloc(zero tile)");
   e = cudaMallocHost(&h->ctl_host, sizeof(Ctl));
   if (e) return bail(e, "cudaMallocHost(ctl)");
   h->rec_cap = h->chunk + 4;
-  e = cudaMalloc(&h->rec_step, h->rec_cap * sizeof(long long));
-  if (!e) e = cudaMalloc(&h->rec_pops, h->rec_cap * q.d_full * sizeof(double));
+  e = pool_alloc(h->device, h->rec_cap * sizeof(long long), reinterpret_cast<void**>(&h->rec_step));
+  if (!e)
+    e = pool_alloc(h->device, h->rec_cap * q.d_full * sizeof(double),
+                   reinterpret_cast<void**>(&h->rec_pops));
   if (!e && q.record_matrices)
-    e = cudaMalloc(&h->rec_mats, h->rec_cap * q.d_full * q.d_full * 2 * sizeof(double));
+    e = pool_alloc(h->device, h->rec_cap * q.d_full * q.d_full * 2 * sizeof(double),
+                   reinterpret_cast<void**>(&h->rec_mats));
   if (e) return bail(e, "cudaMalloc(records)");
 
   KParams& p = h->base;
@@ -535,7 +630,8 @@ int hb_create(const hb_params* P, hb_handle** out) {
 }
 
 static KParams stage_params(hb_handle* h, int stage) {
-  KParams p = h->base;
+  KParams p;
+  std::memcpy(&p, &h->base, sizeof p);  // byte-exact (padding too): GraphCache keys
   double* S = h->buf[0];
   double* Y2 = h->buf[1];
   double* Y3 = h->buf[2];
@@ -574,8 +670,11 @@ static int alloc_state(hb_handle* h, int layout) {
                   "d <= 8, n_matsubara <= 1 and kernel='auto'");
   }
   const size_t bytes = (size_t)(h->n_tiles + 1) * TILE * h->n_planes * elem_size(h);
+  h->buf_bytes = bytes;
   for (auto& b : h->buf) {
-    CK(cudaMalloc(&b, bytes));
+    void* p = nullptr;
+    CK(pool_alloc(h->device, bytes, &p));
+    b = static_cast<double*>(p);
     CK(cudaMemsetAsync(b, 0, bytes, h->stream));
   }
   h->base.hermitian = layout == HB_LAYOUT_HERMITIAN;
@@ -690,8 +789,19 @@ int hb_set_rho0(hb_handle* h, const double* rho0, const double* sink_pops) {
 
 static int ensure_graph(hb_handle* h) {
   if (h->graph && h->graph_layout == h->layout) return HB_OK;
-  if (h->graph) cudaGraphExecDestroy(h->graph);
-  h->graph = nullptr;
+  graph_cache_put(h);
+  std::string key(reinterpret_cast<const char*>(&h->device), sizeof(int));
+  key.append(reinterpret_cast<const char*>(&h->chunk), sizeof(int));
+  for (int s = 1; s <= 4; ++s) {
+    const KParams p = stage_params(h, s);
+    key.append(reinterpret_cast<const char*>(&p), sizeof(KParams));
+  }
+  h->graph_key = key;
+  h->graph = graph_cache_take(key);
+  if (h->graph) {
+    h->graph_layout = h->layout;
+    return HB_OK;
+  }
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   cudaError_t err = cudaSuccess;
