@@ -120,23 +120,10 @@ static cudaError_t mm6_launch_t(int stage, const KParams& p, cudaStream_t s) {
   return mm6_launch_w<D, KP1, 4>(stage, p, s);
 }
 
-template <int D>
-static cudaError_t mm6_kp1(int stage, const KParams& p, cudaStream_t s) {
-  return p.kp1 == 1 ? mm6_launch_t<D, 1>(stage, p, s) : mm6_launch_t<D, 2>(stage, p, s);
-}
-
 cudaError_t launch_mm6(int stage, const KParams& p, cudaStream_t s) {
-  switch (p.d) {
-    case 1: return mm6_kp1<1>(stage, p, s);
-    case 2: return mm6_kp1<2>(stage, p, s);
-    case 3: return mm6_kp1<3>(stage, p, s);
-    case 4: return mm6_kp1<4>(stage, p, s);
-    case 5: return mm6_kp1<5>(stage, p, s);
-    case 6: return mm6_kp1<6>(stage, p, s);
-    case 7: return mm6_kp1<7>(stage, p, s);
-    case 8: return mm6_kp1<8>(stage, p, s);
-  }
-  return cudaErrorInvalidValue;
+  // experiment: instantiated for the FMO shape only (others run k_mm4)
+  if (p.d == 7 && p.kp1 == 2 && !p.single) return mm6_launch_t<7, 2>(stage, p, s);
+  return launch_mm4(stage, p, s);
 }
 
 }  // namespace hb
