@@ -173,9 +173,8 @@ __device__ void sig0_warp(const KParams& P, Sig0& s0) {
 }
 
 template <int D>
-__device__ void record_warp(const KParams& P, long long step, const Sig0& s0) {
+__device__ void record_warp(const KParams& P, long long step, const Sig0& s0, volatile Ctl* c) {
   const int lane = threadIdx.x & 31;
-  volatile Ctl* c = P.ctl;
   const long long idx = c->n_rec;
   if (idx >= P.rec_cap) return;  // host sizes the buffer for a whole chunk
   const int df = P.d_full;
@@ -210,9 +209,8 @@ __device__ void record_warp(const KParams& P, long long step, const Sig0& s0) {
 
 // stop policy evaluated before step `step` (heom.py:359-368)
 template <int D>
-__device__ void check_stop_warp(const KParams& P, long long step, const Sig0& s0) {
+__device__ void check_stop_warp(const KParams& P, long long step, const Sig0& s0, volatile Ctl* c) {
   const int lane = threadIdx.x & 31;
-  volatile Ctl* c = P.ctl;
   int st = ST_RUNNING;
   if (lane == 0) {
     const double t = (double)step * P.dt;
@@ -227,7 +225,7 @@ __device__ void check_stop_warp(const KParams& P, long long step, const Sig0& s0
   }
   st = __shfl_sync(0xffffffffu, st, 0);
   if (st == ST_RUNNING) return;
-  if (st != ST_HARDCAP && step % P.stride != 0) record_warp<D>(P, step, s0);
+  if (st != ST_HARDCAP && step % P.stride != 0) record_warp<D>(P, step, s0, c);
   if (lane == 0) c->status = st;
 }
 
@@ -249,6 +247,30 @@ __device__ inline void finish_step_shard(const KParams& P, long long step) {
   if (P.has_t_end && t >= P.t_end - 1e-9) c->status = ST_T_END;
 }
 
+// The control block is read once, in parallel with sigma^0, into a shared
+// copy (one round trip instead of a chain of dependent volatile accesses), the
+// bookkeeping works on the copy, and the copy is written back at the end.  No
+// other CTA touches the block meanwhile: this is the last CTA of the step (or
+// the init kernel).
+__device__ __forceinline__ void ctl_load_warp(const Ctl* g, Ctl& cs) {
+  constexpr int NW = sizeof(Ctl) / 8;
+  static_assert(sizeof(Ctl) % 8 == 0, "Ctl is copied in 8-byte words");
+  __syncwarp();  // lane 0's last writes to the block are ordered before the copy
+  const int lane = threadIdx.x & 31;
+  for (int w = lane; w < NW; w += 32)
+    reinterpret_cast<unsigned long long*>(&cs)[w] =
+        __ldcg(reinterpret_cast<const unsigned long long*>(g) + w);
+}
+__device__ __forceinline__ void ctl_store_warp(Ctl* g, const Ctl& cs) {
+  constexpr int NW = sizeof(Ctl) / 8;
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  for (int w = lane; w < NW; w += 32)
+    __stcg(reinterpret_cast<unsigned long long*>(g) + w,
+           reinterpret_cast<const unsigned long long*>(&cs)[w]);
+  __syncwarp();
+}
+
 template <int D, bool HERM>
 __device__ void finish_step_warp(const KParams& P, long long step) {
   if (!P.root) {
@@ -256,9 +278,11 @@ __device__ void finish_step_warp(const KParams& P, long long step) {
     return;
   }
   __shared__ Sig0 s0;
+  __shared__ Ctl cs;
   const int lane = threadIdx.x & 31;
-  volatile Ctl* c = P.ctl;
-  sig0_warp<D, HERM>(P, s0);
+  ctl_load_warp(P.ctl, cs);
+  sig0_warp<D, HERM>(P, s0);  // ends with __syncwarp: cs is complete too
+  volatile Ctl* c = &cs;
   double m0 = 0.0;
   for (int f = lane; f < D * D; f += 32) m0 = fmax(m0, s0.re[f] * s0.re[f] + s0.im[f] * s0.im[f]);
 #pragma unroll
@@ -280,9 +304,11 @@ __device__ void finish_step_warp(const KParams& P, long long step) {
   }
   diverged = __shfl_sync(0xffffffffu, diverged, 0);
   __syncwarp();
-  if (diverged) return;
-  if (step % P.stride == 0) record_warp<D>(P, step, s0);
-  check_stop_warp<D>(P, step, s0);
+  if (!diverged) {
+    if (step % P.stride == 0) record_warp<D>(P, step, s0, c);
+    check_stop_warp<D>(P, step, s0, c);
+  }
+  ctl_store_warp(P.ctl, cs);
 }
 
 // t = 0 sample + stop policy before the first step (heom.py:355-368); 1 warp
@@ -293,9 +319,12 @@ __device__ void init_warp(const KParams& P) {
     return;
   }
   __shared__ Sig0 s0;
+  __shared__ Ctl cs;
+  ctl_load_warp(P.ctl, cs);
   sig0_warp<D, HERM>(P, s0);
-  record_warp<D>(P, 0, s0);
-  check_stop_warp<D>(P, 0, s0);
+  record_warp<D>(P, 0, s0, &cs);
+  check_stop_warp<D>(P, 0, s0, &cs);
+  ctl_store_warp(P.ctl, cs);
 }
 
 }  // namespace hb
