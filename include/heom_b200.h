@@ -42,6 +42,7 @@ extern "C" {
 /* ADO orderings on the device (the tables exported are always reference order) */
 #define HB_ORDER_LEX 0         /* pure lexicographic over all tiers (locality)  */
 #define HB_ORDER_REFERENCE 1   /* tier-major lexicographic (hierarchy.py:71-78) */
+#define HB_ORDER_LEX_SPLIT 2   /* lexicographic tiles, top tier last inside a tile */
 
 /* stage-kernel variants */
 #define HB_KERNEL_AUTO 0       /* unrolled thread-per-ADO kernel when the shape allows */

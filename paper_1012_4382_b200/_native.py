@@ -20,7 +20,7 @@ LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 HB_OK, HB_ERR_ARG, HB_ERR_CUDA, HB_DIVERGED, HB_HARDCAP, HB_ERR_RANGE = 0, 1, 2, 3, 4, 5
 HB_STOP_NONE, HB_STOP_T_END, HB_STOP_RESIDUAL = 0, 1, 2
 HB_LAYOUT = {"auto": 0, "hermitian": 1, "general": 2}
-HB_ORDER = {"lex": 0, "reference": 1}
+HB_ORDER = {"lex": 0, "reference": 1, "lex-split": 2}
 HB_KERNEL = {"auto": 0, "generic": 1}
 HB_PREC = {"double": 0, "single": 1}
 

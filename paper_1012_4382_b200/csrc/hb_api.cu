@@ -474,6 +474,8 @@ int hb_create(const hb_params* P, hb_handle** out) {
   if (q.d_full > MAXFULL) return fail(HB_ERR_ARG, "full basis dimension above 16 is not supported");
   if (!(q.dt > 0)) return fail(HB_ERR_ARG, "dt must be > 0");
   if (q.record_stride < 1) return fail(HB_ERR_ARG, "record stride must be >= 1");
+  if (q.ordering < HB_ORDER_LEX || q.ordering > HB_ORDER_LEX_SPLIT)
+    return fail(HB_ERR_ARG, "ordering must be 'lex', 'lex-split' or 'reference'");
   if (q.precision != HB_PREC_DOUBLE && q.precision != HB_PREC_SINGLE)
     return fail(HB_ERR_ARG, "precision must be 'double' or 'single'");
   int nterms = 0;

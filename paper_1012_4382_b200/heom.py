@@ -48,7 +48,8 @@ class PropagationConfig:
       device       CUDA ordinal;
       layout       'auto' (Hermitian-packed when rho0 is exactly Hermitian),
                    'hermitian' or 'general';
-      ordering     device ADO order: 'lex' (locality) or 'reference';
+      ordering     device ADO order: 'lex' (locality), 'lex-split' (lex tiles,
+                   top tier last inside a tile) or 'reference';
       chunk_steps  RK4 steps per CUDA-graph launch (0 = library default);
       kernel       'auto' (unrolled thread-per-ADO kernel when the shape allows)
                    or 'generic' (runtime-shaped tile kernel).
@@ -71,7 +72,7 @@ class PropagationConfig:
     n_matsubara: int = 0
     device: int = 0
     layout: str = "auto"
-    ordering: str = "lex"
+    ordering: str = "lex-split"
     chunk_steps: int = 0
     kernel: str = "auto"
 
@@ -93,7 +94,7 @@ class PropagationConfig:
         if self.layout not in N.HB_LAYOUT:
             raise ValueError("layout must be 'auto', 'hermitian' or 'general'")
         if self.ordering not in N.HB_ORDER:
-            raise ValueError("ordering must be 'lex' or 'reference'")
+            raise ValueError("ordering must be 'lex', 'lex-split' or 'reference'")
         if self.kernel not in N.HB_KERNEL:
             raise ValueError("kernel must be 'auto' or 'generic'")
 

@@ -196,7 +196,7 @@ class ShardedRun:
         self.runs = [DeviceRun(ops, n_max, dt_fs, t_end_fs=t_end_fs, record_stride=record_stride,
                                record_matrices=record_matrices, blowup_norm=blowup_norm,
                                device=devices[q], layout="hermitian", tile_range=rg,
-                               precision=precision)
+                               precision=precision, ordering="lex")
                      for q, rg in enumerate(self.plan.ranges)]
 
     def set_rho0(self, rho0_block, sink_pops):
@@ -260,7 +260,8 @@ class NcclShardedRun:
             if exchange == "crosses" else None
         self.rank, self.world = rank, world
         self.run_ = DeviceRun(ops, n_max, dt_fs, t_end_fs=t_end_fs, record_stride=record_stride,
-                              device=device, layout="hermitian", tile_range=self.plan.ranges[rank])
+                              device=device, layout="hermitian", tile_range=self.plan.ranges[rank],
+                              ordering="lex")
         uid = C.create_string_buffer(128)
         if rank == 0:
             N.check(N.lib().hb_nccl_unique_id(uid), "hb_nccl_unique_id")

@@ -142,7 +142,7 @@ def test_layouts_orderings_kernels_agree(K):
                 record_matrices=True, record_stride=10)
     ref = xf.propagate(FMO, BATH300, RATES, xf.PropagationConfig(**base), 1)
     for layout in ("hermitian", "general"):
-        for ordering in ("lex", "reference"):
+        for ordering in ("lex", "lex-split", "reference"):
             for kernel in ("auto", "generic"):
                 cfg = xf.PropagationConfig(**base, layout=layout, ordering=ordering, kernel=kernel)
                 t = xf.propagate(FMO, BATH300, RATES, cfg, 1)
