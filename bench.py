@@ -192,7 +192,7 @@ def run_reference(args):
 def config_dict(world):
     return {"workload": "FMO 300K N_max=8 K=1 (319770 ADOs), RK4 dt=1fs, one step = whole hierarchy",
             "n_max": N_MAX, "n_matsubara": K_MATS, "n_ado": 319770, "dt_fs": DT,
-            "layout": "hermitian-packed AoSoA, lexicographic tiles (top tier last inside a tile)",
+            "layout": "hermitian-packed AoSoA, tier-major ADO order (the reference's)",
             "l2": "inputs larger than L2 (4 x 125 MB state buffers)",
             "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
 
@@ -257,9 +257,9 @@ def run_b200(args):
     from paper_1012_4382_b200.engine import BlockOperands, DeviceRun
     ops = BlockOperands(system, bath, rates, K_MATS)
     n_tot = xf.hierarchy_size(ops.modes, N_MAX)
-    # HB_BENCH_ORDER (experiments): device ADO order of the timed run ('lex-split' default)
+    # HB_BENCH_ORDER (experiments): device ADO order of the timed run ('reference' default)
     run = DeviceRun(ops, N_MAX, DT, t_end_fs=1e15, record_stride=10 ** 12, device=device,
-                    ordering=os.environ.get("HB_BENCH_ORDER", "lex-split"))
+                    ordering=os.environ.get("HB_BENCH_ORDER", "reference"))
     rho0 = np.zeros((D, D), complex)
     rho0[0, 0] = 1.0
     run.set_rho0(rho0, [0.0, 0.0])

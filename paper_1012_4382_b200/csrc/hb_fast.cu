@@ -1583,16 +1583,16 @@ static cudaError_t mm3_launch(int stage, const KParams& p, cudaStream_t s) {
 
 bool fast_supported(int d, int kp1) { return d >= 1 && d <= 8 && kp1 >= 1 && kp1 <= 2; }
 
-// HB_FAST_VARIANT (experiments): 12 = k_mm4 stage 1 + k_mm8 (TMEM accumulator,
-// hb_mm8.cu) stages 2-4 for d = 7, K + 1 = 2 (default); 11 = k_mm8 everywhere;
-// 7 = k_mm4 (hb_mm4.cu),
+// HB_FAST_VARIANT (experiments): 7 = k_mm4 (hb_mm4.cu, default); 12 = k_mm4
+// stage 1 + k_mm8 (TMEM accumulator, hb_mm8.cu) stages 2-4 for d = 7, K + 1 = 2;
+// 11 = k_mm8 everywhere;
 // 6 = register accumulator + predicated gathers,
 // 5 = mode-major + TMA base tile, 12-pass RK,
 // 4 = mode-major, 1 = sigma in registers, 3 = TMA, 2 = warp-split, 0 = column-streamed
 static int fast_variant() {
   static int v = [] {
     const char* e = getenv("HB_FAST_VARIANT");
-    return e ? atoi(e) : 12;
+    return e ? atoi(e) : 7;
   }();
   return v;
 }

@@ -34,7 +34,9 @@ namespace hb {
 // (timing experiment for the streamed part alone; wrong results); 6 = production
 // with an idle second warp per CTA (half the resident working warps, same L1);
 // 7 = base operands read in phase C instead of bulk-copied to shared memory;
-// 8 = registers capped for 12 resident warps per SM (float path).
+// 8 = registers capped for 12 resident warps per SM (float path);
+// 9 = production (paired-site rounds for tiles without raise links are part of
+// every production variant; 7 runs without them).
 template <class T, int D, int KP1, int STAGE, int VAR>
 __global__ void __launch_bounds__(VAR == 6 ? 64 : 32, VAR == 8 ? 12 : 1) k_mm4(const KParams P) {
   constexpr int NP = D * D;
@@ -76,7 +78,7 @@ __global__ void __launch_bounds__(VAR == 6 ? 64 : 32, VAR == 8 ? 12 : 1) k_mm4(c
   const long long step_next = ctl->step + 1;
   T acc[NP];
   phase_a<T, D, KP1, STAGE, kLate>(P, tile, lane, own, c, sBase, sN, &bar, acc);
-  if (VAR != 5) phase_b_sites<T, D, KP1>(P, lane, c, sUp, sDn, sN, acc);
+  if (VAR != 5) phase_b_sites<T, D, KP1, VAR != 7>(P, lane, c, sUp, sDn, sN, acc);
   double maxa2 = 0.0;
   phase_c_store<T, D, STAGE, kLate>(P, lane, own, sBase, acc, maxa2, sInc);
   if (STAGE == 4) stage4_finish<D>(P, step_next, maxa2);
@@ -150,6 +152,7 @@ static cudaError_t mm4_launch_t(int stage, const KParams& p, cudaStream_t s) {
     if (var == 5) return mm4_launch_b<double, D, KP1, 5>(stage, p, s);
     if (var == 6) return mm4_launch_b<double, D, KP1, 6>(stage, p, s);
     if (var == 7) return mm4_launch_b<double, D, KP1, 7>(stage, p, s);
+    if (var == 9) return mm4_launch_b<double, D, KP1, 9>(stage, p, s);
   }
   return mm4_launch_b<double, D, KP1, 1>(stage, p, s);
 }

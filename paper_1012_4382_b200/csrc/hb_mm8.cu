@@ -72,7 +72,8 @@ struct Mm8Smem {
 // phase C with plain loads instead of a bulk copy into shared memory at kernel
 // start, so a CTA needs 16 KB of shared memory instead of 66 KB and L1 keeps
 // ~200 KB for the gathers; phase A then accumulates only the increment.
-template <int D, int KP1, int STAGE, int MINB, bool LATE>
+// PAIRED: tiles without raise links gather two sites' lower links per round trip
+template <int D, int KP1, int STAGE, int MINB, bool LATE, bool PAIRED = true>
 __global__ void __launch_bounds__(32 * kMm8Warps, MINB) k_mm8(const KParams P) {
   constexpr int NP = D * D;
   constexpr int M = D * KP1;
@@ -188,6 +189,79 @@ __global__ void __launch_bounds__(32 * kMm8Warps, MINB) k_mm8(const KParams P) {
     // ---- phase B: one site's cross at a time: TMEM -> registers, + links, -> TMEM
     const double cbk0 = c * P.b[0], cak0 = c * P.a[0];
     const double cbk1 = KP1 > 1 ? c * P.b[KP1 - 1] : 0.0, cak1 = KP1 > 1 ? c * P.a[KP1 - 1] : 0.0;
+    bool up_any = false;
+#pragma unroll
+    for (int m = 0; m < M; ++m) up_any |= sUp[m][lane] >= 0;
+    if (PAIRED && !__any_sync(0xffffffffu, up_any)) {
+      // no lane has a raise link (a top-tier tile): two sites' lower links per
+      // round trip -- all 4(2d-1) loads issued first, then each site's cross is
+      // read from TMEM, updated and written back
+      constexpr int NC = 2 * D - 1;
+#pragma unroll
+      for (int s0 = 0; s0 < D; s0 += 2) {
+        double g[2][KP1][NC];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int st = s0 + j;
+          if (st >= D) continue;
+#pragma unroll
+          for (int k = 0; k < KP1; ++k) {
+            const int pd = sDn[st * KP1 + k][lane];
+            const double* dn = P.Yin + ((pd >> 5) * TB + (pd & 31));
+            int q = 0;
+#pragma unroll
+            for (int o = 0; o < D; ++o) {
+              const int p0 = o == st ? st : Pk<D>::re(st, o);
+              double v0 = 0.0, v1 = 0.0;
+              if (pd >= 0) v0 = __ldg(dn + p0 * TILE);
+              if (o != st && pd >= 0) v1 = __ldg(dn + (p0 + 1) * TILE);
+              g[j][k][q++] = v0;
+              if (o != st) g[j][k][q++] = v1;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int st = s0 + j;
+          if (st >= D) continue;
+          double x[NP];
+          x[st] = tm_ld2(col(st));
+#pragma unroll
+          for (int o = 0; o < D; ++o)
+            if (o != st) tm_ld4(col(Pk<D>::re(st, o)), x[Pk<D>::re(st, o)], x[Pk<D>::re(st, o) + 1]);
+          tm_wait_ld();
+#pragma unroll
+          for (int k = 0; k < KP1; ++k) {
+            const int m = st * KP1 + k;
+            const double n = sDn[m][lane] >= 0 ? (double)sN[m][lane] : 0.0;
+            const double cb = n * (k == 0 ? cbk0 : cbk1), ca = n * (k == 0 ? cak0 : cak1);
+            int q = 0;
+#pragma unroll
+            for (int o = 0; o < D; ++o) {
+              if (o == st) {
+                x[st] = fma(2.0 * cb, g[j][k][q++], x[st]);
+                continue;
+              }
+              const int pr = Pk<D>::re(st, o), pim = pr + 1;
+              const double dr = g[j][k][q], di = g[j][k][q + 1];
+              q += 2;
+              if (o > st) {
+                x[pr] = fma(cb, dr, fma(-ca, di, x[pr]));
+                x[pim] = fma(cb, di, fma(ca, dr, x[pim]));
+              } else {
+                x[pr] = fma(cb, dr, fma(ca, di, x[pr]));
+                x[pim] = fma(cb, di, fma(-ca, dr, x[pim]));
+              }
+            }
+          }
+          tm_st2(col(st), x[st]);
+#pragma unroll
+          for (int o = 0; o < D; ++o)
+            if (o != st) tm_st4(col(Pk<D>::re(st, o)), x[Pk<D>::re(st, o)], x[Pk<D>::re(st, o) + 1]);
+          tm_wait_st();
+        }
+      }
+    } else
 #pragma unroll
     for (int st = 0; st < D; ++st) {
       double x[NP];  // only the 2D-1 cross planes of st are touched (compile-time indices)

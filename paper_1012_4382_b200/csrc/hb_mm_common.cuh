@@ -210,7 +210,11 @@ __device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, in
 // phase B: the neighbour crosses, one site at a time (2(K+1) links, 2d-1 planes
 // each, all loads of a site independent), absent links predicated off, every
 // term one DFMA into the register accumulator (c folded into the coefficients)
-template <class T, int D, int KP1>
+// PAIRED: a tile none of whose lanes has a raise link (every ADO on the top
+// tier -- whole tiles only in the tier-major order) gathers two sites' lower
+// links per round trip (the same 4(2d-1) loads as one full site), halving the
+// rounds of that tile
+template <class T, int D, int KP1, bool PAIRED = false>
 __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
                                               const int32_t (*sUp)[TILE],
                                               const int32_t (*sDn)[TILE],
@@ -222,6 +226,48 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
   for (int k = 0; k < KP1; ++k) {
     cbk[k] = c * Opd<T>::b(P, k);
     cak[k] = c * Opd<T>::a(P, k);
+  }
+  if (PAIRED) {
+    bool up_any = false;
+#pragma unroll
+    for (int m = 0; m < D * KP1; ++m) up_any |= sUp[m][lane] >= 0;
+    if (!__any_sync(0xffffffffu, up_any)) {
+#pragma unroll
+      for (int s0 = 0; s0 < D; s0 += 2) {
+#pragma unroll
+        for (int st = s0; st < (s0 + 2 < D ? s0 + 2 : D); ++st) {
+#pragma unroll
+          for (int k = 0; k < KP1; ++k) {
+            const int m = st * KP1 + k;
+            const int pd = sDn[m][lane];
+            const bool vd = pd >= 0;
+            const T* dn = yin + ((pd >> 5) * TB + (pd & 31));
+            const T n = vd ? (T)sN[m][lane] : (T)0;
+            const T cb = n * cbk[k], ca = n * cak[k];
+            auto ld = [](const T* q, bool v) -> T {
+              T r = 0;
+              if (v) r = __ldg(q);
+              return r;
+            };
+            acc[st] = fma((T)2 * cb, ld(dn + st * TILE, vd), acc[st]);
+#pragma unroll
+            for (int o = 0; o < D; ++o) {
+              if (o == st) continue;
+              const int pr = Pk<D>::re(st, o), pim = Pk<D>::im(st, o);
+              const T dr = ld(dn + pr * TILE, vd), di = ld(dn + pim * TILE, vd);
+              if (o > st) {
+                acc[pr] = fma(cb, dr, fma(-ca, di, acc[pr]));
+                acc[pim] = fma(cb, di, fma(ca, dr, acc[pim]));
+              } else {
+                acc[pr] = fma(cb, dr, fma(ca, di, acc[pr]));
+                acc[pim] = fma(cb, di, fma(-ca, dr, acc[pim]));
+              }
+            }
+          }
+        }
+      }
+      return;
+    }
   }
 #pragma unroll
   for (int st = 0; st < D; ++st) {

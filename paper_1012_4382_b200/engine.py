@@ -112,7 +112,7 @@ class DeviceRun:
     def __init__(self, ops: BlockOperands, n_max: int, dt_fs: float, t_end_fs=None,
                  residual=None, hard_cap_fs: float = 200_000.0, record_stride: int = 1,
                  record_matrices: bool = False, blowup_norm: float = 1e6, device: int = 0,
-                 layout: str = "auto", ordering: str = "lex-split", chunk_steps: int = 0,
+                 layout: str = "auto", ordering: str = "reference", chunk_steps: int = 0,
                  kernel: str = "auto", tile_range=None, precision: str = "double"):
         N.require_device(device)
         if ops.d > 9:

@@ -48,8 +48,9 @@ class PropagationConfig:
       device       CUDA ordinal;
       layout       'auto' (Hermitian-packed when rho0 is exactly Hermitian),
                    'hermitian' or 'general';
-      ordering     device ADO order: 'lex' (locality), 'lex-split' (lex tiles,
-                   top tier last inside a tile) or 'reference';
+      ordering     device ADO order: 'reference' (tier-major, default: whole
+                   top-tier tiles take the paired-site rounds), 'lex' (locality)
+                   or 'lex-split' (lex tiles, top tier last inside a tile);
       chunk_steps  RK4 steps per CUDA-graph launch (0 = library default);
       kernel       'auto' (unrolled thread-per-ADO kernel when the shape allows)
                    or 'generic' (runtime-shaped tile kernel).
@@ -72,7 +73,7 @@ class PropagationConfig:
     n_matsubara: int = 0
     device: int = 0
     layout: str = "auto"
-    ordering: str = "lex-split"
+    ordering: str = "reference"
     chunk_steps: int = 0
     kernel: str = "auto"
 

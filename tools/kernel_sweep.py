@@ -24,7 +24,7 @@ bath = xf.BathParams.from_timescale(35.0, 166.0, 300.0)
 rates = xf.MarkovRates.from_inverse_ps(2.5, 250.0)
 ops = BlockOperands(system, bath, rates, K)
 run = DeviceRun(ops, n_max, 1.0, t_end_fs=1e15, record_stride=10 ** 12, device=0,
-                ordering=os.environ.get("HB_BENCH_ORDER", "lex-split"),
+                ordering=os.environ.get("HB_BENCH_ORDER", "reference"),
                 precision=os.environ.get("HB_SWEEP_PREC", "double"))
 rho0 = np.zeros((7, 7), complex)
 rho0[0, 0] = 1.0
