@@ -36,7 +36,8 @@ namespace hb {
 // 7 = base operands read in phase C instead of bulk-copied to shared memory;
 // 8 = registers capped for 12 resident warps per SM (float path);
 // 9 = production (paired-site rounds for tiles without raise links are part of
-// every production variant; 7 runs without them).
+// every production variant; 7 runs without them; three sites per round measured
+// the same as two).
 template <class T, int D, int KP1, int STAGE, int VAR>
 __global__ void __launch_bounds__(VAR == 6 ? 64 : 32, VAR == 8 ? 12 : 1) k_mm4(const KParams P) {
   constexpr int NP = D * D;

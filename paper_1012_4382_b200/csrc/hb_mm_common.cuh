@@ -214,7 +214,7 @@ __device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, in
 // tier -- whole tiles only in the tier-major order) gathers two sites' lower
 // links per round trip (the same 4(2d-1) loads as one full site), halving the
 // rounds of that tile
-template <class T, int D, int KP1, bool PAIRED = false>
+template <class T, int D, int KP1, bool PAIRED = false, int GROUP = 2>
 __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
                                               const int32_t (*sUp)[TILE],
                                               const int32_t (*sDn)[TILE],
@@ -233,9 +233,9 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
     for (int m = 0; m < D * KP1; ++m) up_any |= sUp[m][lane] >= 0;
     if (!__any_sync(0xffffffffu, up_any)) {
 #pragma unroll
-      for (int s0 = 0; s0 < D; s0 += 2) {
+      for (int s0 = 0; s0 < D; s0 += GROUP) {
 #pragma unroll
-        for (int st = s0; st < (s0 + 2 < D ? s0 + 2 : D); ++st) {
+        for (int st = s0; st < (s0 + GROUP < D ? s0 + GROUP : D); ++st) {
 #pragma unroll
           for (int k = 0; k < KP1; ++k) {
             const int m = st * KP1 + k;
