@@ -1,7 +1,7 @@
 // Production stage kernel (variant 7, k_mm4): k_mm3's 12-pass RK bookkeeping
 // and register accumulator, re-cut for occupancy and FP64 issue.
 //
-// What the k_mm3 ncu capture (profiles/r1_ncu_k_mm3_*.csv) showed: 254
+// What the k_mm3 ncu capture (profiles/r1_ncu_k_mm3.json) showed: 254
 // registers -> 8 warps per SM, long-scoreboard stalls ~2.5 per issue, and
 // 1,878 FP64 instructions per tile-stage of which 679 DADD and 469 DMUL (the
 // `a*b - c*d` forms were not contracted), plus 350 CS2R zeroing the
@@ -16,7 +16,10 @@
 //     tables ([mode][32] int32 raise/lower, uint8 n) arrive by one bulk copy
 //     group (cp.async.bulk, one mbarrier) at kernel start: no per-lane table
 //     LDG/STS round trip, the raw positions are decoded to element offsets
-//     where they are used.
+//     where they are used;
+//   * a tile none of whose lanes has a raise link (every top-tier tile of the
+//     tier-major order) gathers two sites' lower links per round trip
+//     (phase_b_sites<PAIRED>): 4 dependent L2 round trips instead of 7.
 // T = double (HB_PREC_DOUBLE) or float (HB_PREC_SINGLE: float state, float RHS,
 // heom.py:93-94; bookkeeping, sinks and records stay double).
 // The arithmetic is the reference RHS (_kernels.py:23-58 generalised to K+1
