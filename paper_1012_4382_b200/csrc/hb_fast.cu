@@ -1632,7 +1632,8 @@ template <int D, int KP1>
 static cudaError_t fast_dispatch(int stage, const KParams& p, cudaStream_t s) {
   if constexpr (D == 7) {
     const int v = fast_variant();
-    if (v == 12)  // production: k_mm4 for stage 1, the TMEM-accumulator k_mm8 for 2-4
+    if (v == 13) return launch_mm9(stage, p, s);
+    if (v == 12)  // k_mm4 for stage 1, the TMEM-accumulator k_mm8 for 2-4
       return KP1 == 2 && stage >= 2 ? launch_mm8(stage, p, s) : launch_mm4(stage, p, s);
     if (v == 11) return KP1 == 2 ? launch_mm8(stage, p, s) : launch_mm4(stage, p, s);
     if (v == 9) return launch_mm6(stage, p, s);

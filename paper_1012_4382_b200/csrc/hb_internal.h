@@ -107,6 +107,8 @@ cudaError_t launch_mm5(int stage, const KParams& p, cudaStream_t s);
 cudaError_t launch_mm6(int stage, const KParams& p, cudaStream_t s);
 // hb_mm8.cu: TMEM-accumulator stage kernel (variant 11, d = 7, K + 1 = 2)
 cudaError_t launch_mm8(int stage, const KParams& p, cudaStream_t s);
+// hb_mm9.cu: TMEM accumulator + pipelined gather rounds (variant 13, d = 7, K + 1 = 2)
+cudaError_t launch_mm9(int stage, const KParams& p, cudaStream_t s);
 
 // hb_stage.cu
 cudaError_t launch_stage(int stage, const KParams& p, cudaStream_t s);
