@@ -404,6 +404,11 @@ static GraphCache& graph_cache() {
 }
 constexpr size_t kGraphCacheCap = 8;
 
+// step graphs launched per host synchronisation in hb_run (records buffer sized
+// for all of them)
+constexpr int kGraphsPerSync = 2;
+
+
 static void graph_cache_put(hb_handle* h) {
   if (!h->graph) return;
   GraphCache& G = graph_cache();
@@ -544,7 +549,7 @@ int hb_create(const hb_params* P, hb_handle** out) {
   if (e) return bail(e, "cudaMalloc(zero tile)");
   e = cudaMallocHost(&h->ctl_host, sizeof(Ctl));
   if (e) return bail(e, "cudaMallocHost(ctl)");
-  h->rec_cap = h->chunk + 4;
+  h->rec_cap = (int64_t)kGraphsPerSync * h->chunk + 4;
   e = pool_alloc(h->device, h->rec_cap * sizeof(long long), reinterpret_cast<void**>(&h->rec_step));
   if (!e)
     e = pool_alloc(h->device, h->rec_cap * q.d_full * sizeof(double),
@@ -825,8 +830,10 @@ int hb_run(hb_handle* h, hb_result* res) {
   int rc = ensure_graph(h);
   if (rc) return rc;
   while (h->ctl_host->status == ST_RUNNING) {
-    CK(cudaGraphLaunch(h->graph, h->stream));
-    h->launches += 4LL * h->chunk;
+    // kGraphsPerSync chunks back to back: the device never idles while the host
+    // drains records and relaunches; a chunk enqueued after the stop early-exits
+    for (int g = 0; g < kGraphsPerSync; ++g) CK(cudaGraphLaunch(h->graph, h->stream));
+    h->launches += 4LL * h->chunk * kGraphsPerSync;
     rc = sync_ctl(h);
     if (rc) return rc;
     rc = drain(h);
