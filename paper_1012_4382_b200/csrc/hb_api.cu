@@ -109,6 +109,7 @@ struct hb_handle {
   cudaGraphExec_t graph = nullptr;
   int graph_layout = -1;
   std::string graph_key;  // GraphCache key of `graph`
+  int64_t graph_nodes = 0;  // kernel launches in one replay of `graph`
   std::vector<int64_t> steps;
   std::vector<double> pops, mats;
   int64_t launches = 0;
@@ -396,7 +397,12 @@ static void pool_release(int device, size_t bytes, void* p) {
 // the pool never hands to two live handles).
 struct GraphCache {
   std::mutex mu;
-  std::vector<std::pair<std::string, cudaGraphExec_t>> lru;  // most recent last
+  struct Entry {
+    std::string key;
+    cudaGraphExec_t exec;
+    int64_t nodes;
+  };
+  std::vector<Entry> lru;  // most recent last
 };
 static GraphCache& graph_cache() {
   static GraphCache* c = new GraphCache();
@@ -413,20 +419,21 @@ static void graph_cache_put(hb_handle* h) {
   if (!h->graph) return;
   GraphCache& G = graph_cache();
   std::lock_guard<std::mutex> lk(G.mu);
-  G.lru.emplace_back(h->graph_key, h->graph);
+  G.lru.push_back({h->graph_key, h->graph, h->graph_nodes});
   if (G.lru.size() > kGraphCacheCap) {
-    cudaGraphExecDestroy(G.lru.front().second);
+    cudaGraphExecDestroy(G.lru.front().exec);
     G.lru.erase(G.lru.begin());
   }
   h->graph = nullptr;
 }
 
-static cudaGraphExec_t graph_cache_take(const std::string& key) {
+static cudaGraphExec_t graph_cache_take(const std::string& key, int64_t* nodes) {
   GraphCache& G = graph_cache();
   std::lock_guard<std::mutex> lk(G.mu);
   for (auto it = G.lru.rbegin(); it != G.lru.rend(); ++it)
-    if (it->first == key) {
-      cudaGraphExec_t g = it->second;
+    if (it->key == key) {
+      cudaGraphExec_t g = it->exec;
+      *nodes = it->nodes;
       G.lru.erase(std::next(it).base());
       return g;
     }
@@ -804,7 +811,7 @@ static int ensure_graph(hb_handle* h) {
     key.append(reinterpret_cast<const char*>(&p), sizeof(KParams));
   }
   h->graph_key = key;
-  h->graph = graph_cache_take(key);
+  h->graph = graph_cache_take(key, &h->graph_nodes);
   if (h->graph) {
     h->graph_layout = h->layout;
     return HB_OK;
@@ -817,6 +824,13 @@ static int ensure_graph(hb_handle* h) {
   cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
   if (err) return cuda_fail(err, "capture stage kernels");
   if (e2) return cuda_fail(e2, "cudaStreamEndCapture");
+  size_t nodes = 0;
+  err = cudaGraphGetNodes(g, nullptr, &nodes);
+  if (err) {
+    cudaGraphDestroy(g);
+    return cuda_fail(err, "cudaGraphGetNodes");
+  }
+  h->graph_nodes = (int64_t)nodes;
   err = cudaGraphInstantiate(&h->graph, g, 0);
   cudaGraphDestroy(g);
   if (err) return cuda_fail(err, "cudaGraphInstantiate");
@@ -833,7 +847,7 @@ int hb_run(hb_handle* h, hb_result* res) {
     // kGraphsPerSync chunks back to back: the device never idles while the host
     // drains records and relaunches; a chunk enqueued after the stop early-exits
     for (int g = 0; g < kGraphsPerSync; ++g) CK(cudaGraphLaunch(h->graph, h->stream));
-    h->launches += 4LL * h->chunk * kGraphsPerSync;
+    h->launches += (int64_t)h->graph_nodes * kGraphsPerSync;
     rc = sync_ctl(h);
     if (rc) return rc;
     rc = drain(h);
@@ -940,14 +954,14 @@ int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
   int64_t left = n_steps;
   while (left >= h->chunk) {
     CK(cudaGraphLaunch(h->graph, h->stream));
-    h->launches += 4LL * h->chunk;
+    h->launches += h->graph_nodes;
     left -= h->chunk;
   }
-  for (; left > 0; --left)
-    for (int s = 1; s <= 4; ++s) {
-      CK(launch_stage(s, stage_params(h, s), h->stream));
-      h->launches += 1;
-    }
+  const int64_t per_step = h->graph_nodes / h->chunk;  // kernels per RK4 step
+  for (; left > 0; --left) {
+    for (int s = 1; s <= 4; ++s) CK(launch_stage(s, stage_params(h, s), h->stream));
+    h->launches += per_step;
+  }
   CK(cudaEventRecord(e1, h->stream));
   CK(cudaEventSynchronize(e1));
   float f = 0.f;
@@ -962,9 +976,9 @@ int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
       CK(cudaEventRecord(ev[r * 5], h->stream));
       for (int s = 1; s <= 4; ++s) {
         CK(launch_stage(s, stage_params(h, s), h->stream));
-        h->launches += 1;
         CK(cudaEventRecord(ev[r * 5 + s], h->stream));
       }
+      h->launches += per_step;
     }
     CK(cudaEventSynchronize(ev.back()));
     for (int s = 0; s < 4; ++s) stage_ms[s] = 0.0;

@@ -85,7 +85,47 @@ __global__ void __launch_bounds__(VAR == 6 ? 64 : 32, VAR == 8 ? 12 : 1) k_mm4(c
   if (VAR != 5) phase_b_sites<T, D, KP1, VAR != 7>(P, lane, c, sUp, sDn, sN, acc);
   double maxa2 = 0.0;
   phase_c_store<T, D, STAGE, kLate>(P, lane, own, sBase, acc, maxa2, sInc);
-  if (STAGE == 4) stage4_finish<D>(P, step_next, maxa2);
+  if (STAGE == 4) {
+    if (VAR == 6) {
+      stage4_finish<D>(P, step_next, maxa2);
+    } else if (step_next % 25 == 0) {  // the step bookkeeping runs in k_step_finish
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxa2 = fmax(maxa2, __shfl_xor_sync(0xffffffffu, maxa2, o));
+      if (lane == 0)
+        atomicMax(const_cast<unsigned long long*>(&ctl->maxabs2_bits),
+                  (unsigned long long)__double_as_longlong(maxa2));
+    }
+  }
+}
+
+// The per-step bookkeeping (sinks heom.py:382-383, guard heom.py:386-389,
+// records, stop policy) as its own one-warp kernel after stage 4, chained by
+// PDL: it waits for the stage-4 grid to complete and flush, so the stage
+// kernels need no per-CTA fence and no contended last-CTA election counter
+// (each of those cost every CTA a round trip before it could retire).
+template <int D>
+__global__ void __launch_bounds__(32, 1) k_step_finish(const KParams P) {
+  volatile Ctl* ctl = P.ctl;
+  pdl_wait();
+  if (ctl->status != ST_RUNNING) return;
+  pdl_release();
+  const long long step_next = ctl->step + 1;
+  if (threadIdx.x == 0) ctl->launches = ctl->launches + 5;
+  finish_step_warp<D, true>(P, step_next);
+}
+
+template <int D>
+static cudaError_t finish_go(const KParams& p, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_step_finish<D>, p);
 }
 
 // HB_MM4_PAD (experiments): unused dynamic shared memory per CTA, to lower the
@@ -128,7 +168,11 @@ static cudaError_t mm4_launch_b(int stage, const KParams& p, cudaStream_t s) {
     case 1: return mm4_go<T, D, KP1, 1, VAR>(p, s);
     case 2: return mm4_go<T, D, KP1, 2, VAR>(p, s);
     case 3: return mm4_go<T, D, KP1, 3, VAR>(p, s);
-    case 4: return mm4_go<T, D, KP1, 4, VAR>(p, s);
+    case 4: {
+      const cudaError_t e = mm4_go<T, D, KP1, 4, VAR>(p, s);
+      if (e != cudaSuccess || VAR == 6) return e;
+      return finish_go<D>(p, s);
+    }
   }
   return cudaErrorInvalidValue;
 }

@@ -368,7 +368,10 @@ __device__ __forceinline__ void stage4_finish(const KParams& P, long long step_n
       atomicMax(const_cast<unsigned long long*>(&ctl->maxabs2_bits),
                 (unsigned long long)__double_as_longlong(maxa2));
   }
-  __threadfence();
+  // the last CTA's bookkeeping reads sigma^0 and the stage-4 sink rates (both
+  // written by the CTA holding tile 0) and, every 25 steps, the max|x|^2 atomics:
+  // only those writes must be visible before the election counter moves
+  if (step_next % 25 == 0 || (P.tile_begin == 0 && blockIdx.x == 0)) __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned prev = atomicAdd(const_cast<unsigned*>(&ctl->blocks_done), 1u);
