@@ -98,6 +98,73 @@ __global__ void __launch_bounds__(VAR == 6 ? 64 : 32, VAR == 8 ? 12 : 1) k_mm4(c
   }
 }
 
+// Split CTAs for grids under about one wave (small hierarchies, where a stage is
+// the latency of one tile's chain of dependent round trips, not bandwidth): two
+// warps per tile.  Warp 0 runs phase A (own ADO, commutator, damping) and the
+// crosses of sites [0, D/2); warp 1 gathers sites [D/2, D) into its own
+// accumulator and hands it over through shared memory; warp 0 stores.  Same
+// arithmetic as k_mm4 (the second accumulator is added once per element before
+// the store, so the sum order differs from k_mm4's by that one regrouping).
+template <class T, int D, int KP1, int STAGE>
+__global__ void __launch_bounds__(64, 1) k_mm4s(const KParams P) {
+  constexpr int NP = D * D;
+  constexpr int M = D * KP1;
+  constexpr int SPLIT = D / 2;
+  constexpr bool kInc = kIncScheme<T>;
+  __shared__ __align__(128) T sBase[STAGE >= 2 || kInc ? NP : 1][TILE];
+  __shared__ __align__(128) T sInc[kInc && (STAGE == 2 || STAGE == 4) ? NP : 1][TILE];
+  __shared__ __align__(128) T sX[NP][TILE];
+  __shared__ __align__(16) int32_t sUp[M][TILE];
+  __shared__ __align__(16) int32_t sDn[M][TILE];
+  __shared__ __align__(16) uint8_t sN[M][TILE];
+  __shared__ __align__(8) uint64_t bar;
+
+  volatile Ctl* ctl = P.ctl;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tile = P.tile_begin + blockIdx.x;
+  const int own = tile * (NP * TILE) + lane;
+  const T c = (T)(STAGE == 4 ? P.dt / 6.0 : P.coef);
+
+  if (warp == 0)
+    tile_prologue<T, D, KP1, STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0], &sN[0][0],
+                                    &bar, true, &sInc[0][0], true);
+  __syncthreads();  // barrier initialised before warp 1 waits on it
+  pdl_wait();
+  if (warp == 0) tile_prologue_late<T, D, STAGE>(P, tile, &sInc[0][0], &bar);
+  if (ctl->status != ST_RUNNING) {
+    mbar_wait(&bar, 0);  // no bulk copy may land after the CTA has exited
+    return;
+  }
+  pdl_release();
+  const long long step_next = ctl->step + 1;
+  T acc[NP];
+  if (warp == 0) {
+    phase_a<T, D, KP1, STAGE>(P, tile, lane, own, c, sBase, sN, &bar, acc);
+    phase_b_sites<T, D, KP1, true, 2, 0, SPLIT>(P, lane, c, sUp, sDn, sN, acc);
+  } else {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) acc[p] = 0;
+    mbar_wait(&bar, 0);
+    phase_b_sites<T, D, KP1, true, 2, SPLIT, D>(P, lane, c, sUp, sDn, sN, acc);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) sX[p][lane] = acc[p];
+  }
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) acc[p] += sX[p][lane];
+  double maxa2 = 0.0;
+  phase_c_store<T, D, STAGE, false>(P, lane, own, sBase, acc, maxa2, sInc);
+  if (STAGE == 4 && step_next % 25 == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxa2 = fmax(maxa2, __shfl_xor_sync(0xffffffffu, maxa2, o));
+    if (lane == 0)
+      atomicMax(const_cast<unsigned long long*>(&ctl->maxabs2_bits),
+                (unsigned long long)__double_as_longlong(maxa2));
+  }
+}
+
 // The per-step bookkeeping (sinks heom.py:382-383, guard heom.py:386-389,
 // records, stop policy) as its own one-warp kernel after stage 4, chained by
 // PDL: it waits for the stage-4 grid to complete and flush, so the stage
@@ -162,8 +229,48 @@ static cudaError_t mm4_go(const KParams& p, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, k_mm4<T, D, KP1, STAGE, VAR>, p);
 }
 
+template <class T, int D, int KP1, int STAGE>
+static cudaError_t mm4s_go(const KParams& p, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.n_tiles);
+  cfg.blockDim = dim3(64);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = mm4_pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_mm4s<T, D, KP1, STAGE>, p);
+}
+
+// HB_SPLIT_TILES (experiment): grids of at most this many tiles run the split CTAs
+// (k_mm4s); off by default (measured no faster)
+static int split_tiles() {
+  static const int v = [] {
+    const char* e = getenv("HB_SPLIT_TILES");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <class T, int D, int KP1>
+static cudaError_t mm4s_launch(int stage, const KParams& p, cudaStream_t s) {
+  switch (stage) {
+    case 1: return mm4s_go<T, D, KP1, 1>(p, s);
+    case 2: return mm4s_go<T, D, KP1, 2>(p, s);
+    case 3: return mm4s_go<T, D, KP1, 3>(p, s);
+    case 4: {
+      const cudaError_t e = mm4s_go<T, D, KP1, 4>(p, s);
+      if (e != cudaSuccess) return e;
+      return finish_go<D>(p, s);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <class T, int D, int KP1, int VAR>
 static cudaError_t mm4_launch_b(int stage, const KParams& p, cudaStream_t s) {
+  if (VAR == 1 && D >= 2 && p.n_tiles <= split_tiles()) return mm4s_launch<T, D, KP1>(stage, p, s);
   switch (stage) {
     case 1: return mm4_go<T, D, KP1, 1, VAR>(p, s);
     case 2: return mm4_go<T, D, KP1, 2, VAR>(p, s);

@@ -214,7 +214,9 @@ __device__ __forceinline__ bool phase_a(const KParams& P, int tile, int lane, in
 // tier -- whole tiles only in the tier-major order) gathers two sites' lower
 // links per round trip (the same 4(2d-1) loads as one full site), halving the
 // rounds of that tile
-template <class T, int D, int KP1, bool PAIRED = false, int GROUP = 2>
+// [S0, S1): the sites this warp gathers (k_mm4's split CTAs give a tile's sites
+// to two warps)
+template <class T, int D, int KP1, bool PAIRED = false, int GROUP = 2, int S0 = 0, int S1 = D>
 __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
                                               const int32_t (*sUp)[TILE],
                                               const int32_t (*sDn)[TILE],
@@ -233,9 +235,9 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
     for (int m = 0; m < D * KP1; ++m) up_any |= sUp[m][lane] >= 0;
     if (!__any_sync(0xffffffffu, up_any)) {
 #pragma unroll
-      for (int s0 = 0; s0 < D; s0 += GROUP) {
+      for (int s0 = S0; s0 < S1; s0 += GROUP) {
 #pragma unroll
-        for (int st = s0; st < (s0 + GROUP < D ? s0 + GROUP : D); ++st) {
+        for (int st = s0; st < (s0 + GROUP < S1 ? s0 + GROUP : S1); ++st) {
 #pragma unroll
           for (int k = 0; k < KP1; ++k) {
             const int m = st * KP1 + k;
@@ -270,7 +272,7 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
     }
   }
 #pragma unroll
-  for (int st = 0; st < D; ++st) {
+  for (int st = S0; st < S1; ++st) {
 #pragma unroll
     for (int k = 0; k < KP1; ++k) {
       const int m = st * KP1 + k;
