@@ -307,6 +307,18 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c,
   }
 }
 
+// HB_ST_CS (build-time experiment): 1 = B (read two stages later) stored
+// evict-first (st.global.cs); 2 = the stage output too; 0 = plain stores
+#ifndef HB_ST_CS
+#define HB_ST_CS 0
+#endif
+template <class T> __device__ __forceinline__ void st_y(T* q, T v) {
+  if (HB_ST_CS >= 2) __stcs(q, v); else *q = v;
+}
+template <class T> __device__ __forceinline__ void st_bb(T* q, T v) {
+  if (HB_ST_CS >= 1) __stcs(q, v); else *q = v;
+}
+
 template <class T, int D, int STAGE, bool LATE = false>
 __device__ __forceinline__ void phase_c_store(const KParams& P, int lane, int own,
                                               T (*sBase)[TILE], T (&acc)[D * D],
@@ -339,8 +351,8 @@ __device__ __forceinline__ void phase_c_store(const KParams& P, int lane, int ow
       acc[p] = STAGE == 4 ? sg + (sInc[p][lane] + a) : sg + a;
       st_out<T>(P)[own + p * TILE] = acc[p];
     } else {
-      st_out<T>(P)[own + p * TILE] = acc[p];
-      if (STAGE == 2) st_b<T>(P)[own + p * TILE] = fma(two3, acc[p], sBase[p][lane]);
+      st_y(st_out<T>(P) + own + p * TILE, acc[p]);
+      if (STAGE == 2) st_bb(st_b<T>(P) + own + p * TILE, fma(two3, acc[p], sBase[p][lane]));
     }
   }
   if (STAGE == 4) {  // max |y|^2 per element (diagonal planes are real)
