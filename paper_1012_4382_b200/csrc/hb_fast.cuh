@@ -67,4 +67,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// the same copy with an L2 evict-last policy (build-time experiment HB_TBL_KEEP:
+// the link tables, re-read every stage, kept in L2 against the streamed state)
+__device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, unsigned bytes,
+                                              uint64_t* bar) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 }  // namespace hb

@@ -63,6 +63,12 @@ struct MmSmem {
 template <class T>
 constexpr bool kIncScheme = std::is_same<T, float>::value;
 
+// HB_TBL_KEEP (build-time experiment): link-table bulk copies with an L2
+// evict-last policy
+#ifndef HB_TBL_KEEP
+#define HB_TBL_KEEP 0
+#endif
+
 template <class T, int D, int KP1, int STAGE>
 __device__ __forceinline__ void tile_prologue(const KParams& P, int tile, T* sBase,
                                               int32_t* sUp, int32_t* sDn, uint8_t* sN,
@@ -81,9 +87,15 @@ __device__ __forceinline__ void tile_prologue(const KParams& P, int tile, T* sBa
     mbar_expect_tx(bar, 2 * LB + NB + (STAGE >= 2 ? TB * (unsigned)sizeof(T) : 0u) +
                             (kLoadInc ? TB * (unsigned)sizeof(T) : 0u));
     const size_t gt = (size_t)tile * M * TILE;
+#if HB_TBL_KEEP
+    bulk_g2s_keep(sUp, P.plus + gt, LB, bar);
+    bulk_g2s_keep(sDn, P.minus + gt, LB, bar);
+    bulk_g2s_keep(sN, P.nvec + gt, NB, bar);
+#else
     bulk_g2s(sUp, P.plus + gt, LB, bar);
     bulk_g2s(sDn, P.minus + gt, LB, bar);
     bulk_g2s(sN, P.nvec + gt, NB, bar);
+#endif
     if (STAGE >= 2)
       bulk_g2s(sBase, (STAGE == 4 && !kInc ? st_b<T>(P) : st_sig<T>(P)) + (size_t)tile * TB,
                TB * (unsigned)sizeof(T), bar);
