@@ -169,6 +169,15 @@ void hb_destroy(hb_handle* h);
  * Hermitian (diagonal imaginary parts zero), else GENERAL. */
 int hb_set_rho0(hb_handle* h, const double* rho0_block, const double* sink_pops);
 
+/* The whole hierarchy state instead of rho0 (auxiliaries included): sig is
+ * (n_tot,d,d) complex in the reference order (hierarchy.py:71-78), sink_pops
+ * n_sinks.  Otherwise as hb_set_rho0 (layout AUTO: HERMITIAN if every ADO is
+ * exactly Hermitian).  The reference's propagate_from accepts only rho0
+ * (heom.py:286-311, auxiliaries zero); this entry point is its state-restart
+ * counterpart, used to pin the production kernel on every ADO against the
+ * oracle (the full-state check of test_heom.py:120-130).  Unsharded handles only. */
+int hb_set_state(hb_handle* h, const double* sig, const double* sink_pops);
+
 /* Run until a stop policy fires (heom.py:358-391).  Returns HB_OK with
  * res->stop_reason set, HB_DIVERGED (res->steps = step whose guard fired) or
  * HB_HARDCAP. */
@@ -196,8 +205,15 @@ int hb_get_sigma0(hb_handle* h, double* sig0, double* sink_pops);
  * each stage kernel, measured with events around individual launches. */
 int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms_or_null);
 
-/* Device-side launch count of product kernels since hb_create. */
+/* Product kernels that did work since hb_create: host-launched ones plus the
+ * step kernels counted on the device (as of the handle's last synchronisation). */
 int64_t hb_launch_count(hb_handle* h);
+
+/* Frees the idle device buffers the library pools between handles (state
+ * buffers of finished runs are kept per (device, size) up to 24 GiB so that a
+ * repeated propagate() of the same shape skips cudaMalloc; an allocation that
+ * fails also trims the pool and retries).  Live handles are untouched. */
+void hb_pool_trim(void);
 
 /* ---- Sharding (new, no reference counterpart) ----
  * A handle created with tile_begin/tile_count computes only that contiguous

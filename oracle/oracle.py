@@ -233,7 +233,7 @@ def rhs_from_arrays(sig, h, site_of, plus, minus, nvec, n_sites, kp1, nu, a, b, 
 
 
 def propagate_from(system, bath, rates, config, rho0, n_matsubara=None, problem=None,
-                   max_records=None):
+                   max_records=None, init_state=None):
     """heom.py:286-406 on the C oracle.  Returns a dict shaped like Trajectory
     (times_fs, populations, final_rho, matrices, stop_reason) or raises
     RuntimeError('diverged' / 'hardcap' ...) carrying the reference message."""
@@ -243,6 +243,8 @@ def propagate_from(system, bath, rates, config, rho0, n_matsubara=None, problem=
     rho0 = np.asarray(rho0, dtype=complex)
     sig = np.zeros((pb.n_tot, pb.d, pb.d), np.complex128)
     sig[0] = rho0[np.ix_(pb.block, pb.block)]
+    if init_state is not None:  # the whole hierarchy (reference order), auxiliaries included
+        sig[...] = init_state
     sink_pops = np.array([float(rho0[s, s].real) for s in pb.sinks] or [0.0])
     nterms = np.array([len(t) for t in pb.sink_terms] or [0], np.int32)
     rate = np.array([r for t in pb.sink_terms for r, _ in t] or [0.0])

@@ -98,7 +98,6 @@ struct hb_handle {
   int n_planes = 0;
   double* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // sigma, Y2, Y3, Y4, B
   size_t buf_bytes = 0;
-  double* zero_tile = nullptr;  // never written: target of absent links
   Ctl* ctl = nullptr;
   Ctl* ctl_host = nullptr;  // pinned
   long long* rec_step = nullptr;
@@ -109,10 +108,13 @@ struct hb_handle {
   cudaGraphExec_t graph = nullptr;
   int graph_layout = -1;
   std::string graph_key;  // GraphCache key of `graph`
-  int64_t graph_nodes = 0;  // kernel launches in one replay of `graph`
+  int64_t graph_nodes = 0;  // kernel launches in one body (WHILE) / replay (plain) of `graph`
+  bool graph_while = false;  // `graph` is a WHILE node over a body of `chunk` steps
+  long long loop_iters = 1;  // WHILE-body iterations per graph launch
   std::vector<int64_t> steps;
   std::vector<double> pops, mats;
-  int64_t launches = 0;
+  int64_t launches = 0;       // host-launched kernels (init, pack/unpack)
+  int64_t launches_base = 0;  // device-counted step kernels of earlier runs of the handle
   bool ready = false;  // rho0 set
   int own_begin = 0, own_count = 0;  // sharding: owned tile range
   void* nccl_comm = nullptr;
@@ -362,6 +364,24 @@ static BufPool& buf_pool() {
 }
 constexpr size_t kPoolCap = size_t(24) << 30;
 
+static void pool_trim_device(int device) {
+  BufPool& P = buf_pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  for (auto it = P.idle.begin(); it != P.idle.end();) {
+    if (device < 0 || it->first.first == device) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(it->first.first);
+      cudaFree(it->second);
+      cudaSetDevice(cur);
+      P.cached -= it->first.second;
+      it = P.idle.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
 static cudaError_t pool_alloc(int device, size_t bytes, void** out) {
   {
     BufPool& P = buf_pool();
@@ -374,7 +394,13 @@ static cudaError_t pool_alloc(int device, size_t bytes, void** out) {
       return cudaSuccess;
     }
   }
-  return cudaMalloc(out, bytes);
+  cudaError_t e = cudaMalloc(out, bytes);
+  if (e == cudaErrorMemoryAllocation) {  // idle pooled buffers may be what is missing
+    cudaGetLastError();
+    pool_trim_device(device);
+    e = cudaMalloc(out, bytes);
+  }
+  return e;
 }
 
 static void pool_release(int device, size_t bytes, void* p) {
@@ -387,6 +413,70 @@ static void pool_release(int device, size_t bytes, void* p) {
   P.idle.insert({{device, bytes}, p});
   P.cached += bytes;
 }
+
+// Streams and pinned control blocks are pooled too: propagate() creates a
+// handle per call, and cudaStreamCreate / cudaMallocHost cost tens of
+// microseconds to milliseconds each.
+struct HostPool {
+  std::mutex mu;
+  std::multimap<int, cudaStream_t> streams;
+  std::vector<Ctl*> pinned;
+};
+static HostPool& host_pool() {
+  static HostPool* p = new HostPool();
+  return *p;
+}
+
+static cudaError_t stream_acquire(int device, cudaStream_t* s) {
+  {
+    HostPool& H = host_pool();
+    std::lock_guard<std::mutex> lk(H.mu);
+    auto it = H.streams.find(device);
+    if (it != H.streams.end()) {
+      *s = it->second;
+      H.streams.erase(it);
+      return cudaSuccess;
+    }
+  }
+  return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+}
+
+static void stream_release(int device, cudaStream_t s) {
+  HostPool& H = host_pool();
+  std::lock_guard<std::mutex> lk(H.mu);
+  if (H.streams.count(device) >= 64) {
+    cudaStreamDestroy(s);
+    return;
+  }
+  H.streams.insert({device, s});
+}
+
+static cudaError_t pinned_acquire(Ctl** c) {
+  {
+    HostPool& H = host_pool();
+    std::lock_guard<std::mutex> lk(H.mu);
+    if (!H.pinned.empty()) {
+      *c = H.pinned.back();
+      H.pinned.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaMallocHost(reinterpret_cast<void**>(c), sizeof(Ctl));
+}
+
+static void pinned_release(Ctl* c) {
+  HostPool& H = host_pool();
+  std::lock_guard<std::mutex> lk(H.mu);
+  if (H.pinned.size() >= 256) {
+    cudaFreeHost(c);
+    return;
+  }
+  H.pinned.push_back(c);
+}
+
+// Frees every idle pooled device buffer (all devices).  Buffers of live handles
+// are untouched.
+void hb_pool_trim(void) { pool_trim_device(-1); }
 
 // Instantiated step graphs, keyed by the bytes of the four stages' kernel
 // parameters (+ chunk and device): instantiating 4 x chunk_steps kernel nodes
@@ -413,6 +503,9 @@ constexpr size_t kGraphCacheCap = 8;
 // step graphs launched per host synchronisation in hb_run (records buffer sized
 // for all of them)
 constexpr int kGraphsPerSync = 2;
+// RK4 steps per WHILE-body (PDL-chained inside a body; a run stops within the
+// body of its stop step)
+constexpr int kDefaultBodySteps = 4;
 
 
 static void graph_cache_put(hb_handle* h) {
@@ -460,16 +553,14 @@ void hb_destroy(hb_handle* h) {
   free_state(h);
   free_halo(h);
   h->graph_ref.reset();
-  const size_t zbytes = (size_t)2 * MAXD * MAXD * TILE * sizeof(double);
   if (h->ctl) pool_release(h->device, sizeof(Ctl), h->ctl);
-  if (h->zero_tile) pool_release(h->device, zbytes, h->zero_tile);
-  cudaFreeHost(h->ctl_host);
+  if (h->ctl_host) pinned_release(h->ctl_host);
   if (h->rec_step) pool_release(h->device, h->rec_cap * sizeof(long long), h->rec_step);
   if (h->rec_pops) pool_release(h->device, h->rec_cap * h->prm.d_full * sizeof(double), h->rec_pops);
   if (h->rec_mats)
     pool_release(h->device, h->rec_cap * h->prm.d_full * h->prm.d_full * 2 * sizeof(double),
                  h->rec_mats);
-  if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->stream) stream_release(h->device, h->stream);
   delete h;
 }
 
@@ -503,7 +594,14 @@ int hb_create(const hb_params* P, hb_handle** out) {
   h->device = q.device;
   h->modes = modes;
   h->n_tot = (int)n_tot;
-  h->chunk = q.chunk_steps > 0 ? q.chunk_steps : 64;
+  // steps per CUDA-graph body (ensure_graph); a graph launch runs up to
+  // loop_iters bodies: 128 records' worth of steps at stride 1, more for sparse
+  // records (fewer host synchronisations), at most 16,384
+  h->chunk = q.chunk_steps > 0 ? q.chunk_steps : kDefaultBodySteps;
+  {
+    const int64_t want = std::max<int64_t>(h->chunk, std::min<int64_t>(128 * q.record_stride, 16384));
+    h->loop_iters = (want + h->chunk - 1) / h->chunk;
+  }
   const int d = q.d;
   h->h.assign(q.h, q.h + d * d);
   h->decay.assign(q.decay, q.decay + d);
@@ -529,7 +627,7 @@ int hb_create(const hb_params* P, hb_handle** out) {
   };
   cudaError_t e = cudaSetDevice(h->device);
   if (e) return bail(e, "cudaSetDevice");
-  e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  e = stream_acquire(h->device, &h->stream);
   if (e) return bail(e, "cudaStreamCreate");
   e = shared_graph(modes, q.n_max, q.ordering, h->device, h->stream, &h->graph_ref);
   if (e) return bail(e, "build_graph");
@@ -550,13 +648,11 @@ int hb_create(const hb_params* P, hb_handle** out) {
   // reuse a cached instantiated CUDA graph (ensure_graph)
   e = pool_alloc(h->device, sizeof(Ctl), reinterpret_cast<void**>(&h->ctl));
   if (e) return bail(e, "cudaMalloc(ctl)");
-  const size_t zbytes = (size_t)2 * MAXD * MAXD * TILE * sizeof(double);
-  e = pool_alloc(h->device, zbytes, reinterpret_cast<void**>(&h->zero_tile));
-  if (!e) e = cudaMemsetAsync(h->zero_tile, 0, zbytes, h->stream);
-  if (e) return bail(e, "cudaMalloc(zero tile)");
-  e = cudaMallocHost(&h->ctl_host, sizeof(Ctl));
+  e = pinned_acquire(&h->ctl_host);
   if (e) return bail(e, "cudaMallocHost(ctl)");
-  h->rec_cap = (int64_t)kGraphsPerSync * h->chunk + 4;
+  std::memset(h->ctl_host, 0, sizeof(Ctl));  // pooled: may hold a previous handle's block
+  // records of kGraphsPerSync launches between two drains (+ the final sample)
+  h->rec_cap = (int64_t)kGraphsPerSync * (h->loop_iters * h->chunk / q.record_stride + 2) + 4;
   e = pool_alloc(h->device, h->rec_cap * sizeof(long long), reinterpret_cast<void**>(&h->rec_step));
   if (!e)
     e = pool_alloc(h->device, h->rec_cap * q.d_full * sizeof(double),
@@ -601,14 +697,14 @@ int hb_create(const hb_params* P, hb_handle** out) {
   p.minus = h->gt.minus_t;
   p.nvec = h->gt.nvec_t;
   p.damp_plane = nullptr;
-  p.zero_tile = h->zero_tile;
-  {
-    const char* e = getenv("HB_PREFETCH");
-    p.prefetch = e ? atoi(e) : 1;
-    const char* g = getenv("HB_DEBUG_NOGATHER");
-    p.debug = g ? atoi(g) : 0;
-    const char* d = getenv("HB_PFD");
-    p.pf_dist = d ? atoi(d) : 0;
+  p.tile_list = nullptr;
+  // tier-major order: the top tier (no raise links) is the last
+  // C(N_max + M - 1, N_max) positions; tiles wholly inside it skip the raise table
+  p.top_tile = h->n_tiles;
+  if (q.ordering == HB_ORDER_REFERENCE) {
+    const int64_t top_count = hierarchy_size(modes - 1, q.n_max);  // |n| = N_max exactly
+    const int64_t first_top = n_tot - top_count;
+    p.top_tile = (int)((first_top + TILE - 1) / TILE);
   }
   p.dt = q.dt;
   p.ctl = h->ctl;
@@ -677,7 +773,7 @@ static int alloc_state(hb_handle* h, int layout) {
   if (h->base.single) {
     bool identity = h->prm.n_sites == d;
     for (int i = 0; i < d; ++i) identity = identity && h->site_of[i] == i;
-    if (layout != HB_LAYOUT_HERMITIAN || !identity || !fast_supported(d, h->prm.kp1) ||
+    if (layout != HB_LAYOUT_HERMITIAN || !identity || !mm4_supported(d, h->prm.kp1) ||
         h->prm.kernel_variant != HB_KERNEL_AUTO)
       return fail(HB_ERR_ARG,
                   "precision='single' needs a Hermitian rho0, every block level a site, "
@@ -697,9 +793,8 @@ static int alloc_state(hb_handle* h, int layout) {
   for (int i = 0; i < d; ++i) identity = identity && h->site_of[i] == i;
   // the unrolled kernels address a buffer with int32 element offsets
   const bool fits32 = (h->n_tiles + 1) * (int64_t)TILE * h->n_planes < INT32_MAX;
-  h->base.fast = h->base.hermitian && identity && fast_supported(d, h->prm.kp1) &&
+  h->base.fast = h->base.hermitian && identity && mm4_supported(d, h->prm.kp1) &&
                  h->prm.kernel_variant == HB_KERNEL_AUTO && fits32;
-  if (h->base.fast) CK(configure_fast(h->base));
   CK(configure_stages(h->base));
   return HB_OK;
 }
@@ -732,6 +827,29 @@ static int drain(hb_handle* h) {
 static int sync_ctl(hb_handle* h) {
   CK(cudaMemcpyAsync(h->ctl_host, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  return HB_OK;
+}
+
+// (re)starts the run on the state in buffer 0: control block, t = 0 sample and
+// stop policy before the first step (heom.py:355-368)
+static int start_run(hb_handle* h, const double* sink_pops) {
+  h->launches_base += h->ctl_host->launches;  // the device count restarts with the block
+  Ctl c{};
+  c.status = ST_RUNNING;
+  for (int s = 0; s < h->prm.n_sinks; ++s) c.sink_pops[s] = sink_pops[s];
+  std::memcpy(h->ctl_host, &c, sizeof c);
+  CK(cudaMemcpyAsync(h->ctl, h->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
+  h->steps.clear();
+  h->pops.clear();
+  h->mats.clear();
+  KParams p = stage_params(h, 4);
+  CK(launch_init(p, h->stream));
+  h->launches += 1;
+  int rc = sync_ctl(h);
+  if (rc) return rc;
+  rc = drain(h);
+  if (rc) return rc;
+  h->ready = true;
   return HB_OK;
 }
 
@@ -782,30 +900,115 @@ int hb_set_rho0(hb_handle* h, const double* rho0, const double* sink_pops) {
     CK(cudaMemcpyAsync(h->buf[0], tile0.data(), tile0.size() * sizeof(double),
                        cudaMemcpyHostToDevice, h->stream));
   }
-  Ctl c{};
-  c.status = ST_RUNNING;
-  for (int s = 0; s < h->prm.n_sinks; ++s) c.sink_pops[s] = sink_pops[s];
-  std::memcpy(h->ctl_host, &c, sizeof c);
-  CK(cudaMemcpyAsync(h->ctl, h->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
-  h->steps.clear();
-  h->pops.clear();
-  h->mats.clear();
-  KParams p = stage_params(h, 4);
-  CK(launch_init(p, h->stream));
+  return start_run(h, sink_pops);
+}
+
+int hb_set_state(hb_handle* h, const double* sig, const double* sink_pops) {
+  if (!h) return fail(HB_ERR_ARG, "null handle");
+  if (h->own_begin != 0 || h->own_count != h->n_tiles)
+    return fail(HB_ERR_ARG, "hb_set_state needs an unsharded handle");
+  CK(cudaSetDevice(h->device));
+  const int d = h->prm.d;
+  int layout = h->prm.layout;
+  if (layout == HB_LAYOUT_AUTO) {  // Hermitian-packed only if every ADO is exactly Hermitian
+    bool herm = true;
+    for (int64_t k = 0; k < h->n_tot && herm; ++k) {
+      const double* m = sig + (size_t)k * d * d * 2;
+      for (int i = 0; i < d && herm; ++i)
+        for (int j = i; j < d; ++j)
+          if (m[2 * (i * d + j)] != m[2 * (j * d + i)] ||
+              m[2 * (i * d + j) + 1] != -m[2 * (j * d + i) + 1]) {
+            herm = false;
+            break;
+          }
+    }
+    layout = herm ? HB_LAYOUT_HERMITIAN : HB_LAYOUT_GENERAL;
+  }
+  int rc = alloc_state(h, layout);
+  if (rc) return rc;
+  const size_t ref_bytes = (size_t)h->n_tot * d * d * 2 * sizeof(double);
+  DevBuf tmp;
+  CK(tmp.alloc(ref_bytes));
+  CK(cudaMemcpyAsync(tmp.p, sig, ref_bytes, cudaMemcpyHostToDevice, h->stream));
+  CK(launch_pack(h->base, tmp.as<double>(), h->gt.dev2ref, h->buf[0], h->stream));
   h->launches += 1;
-  rc = sync_ctl(h);
-  if (rc) return rc;
-  rc = drain(h);
-  if (rc) return rc;
-  h->ready = true;
+  return start_run(h, sink_pops);  // synchronises before tmp is freed
+}
+
+// One graph launch = a CUDA-graph WHILE node whose body is `chunk` RK4 steps
+// (5 PDL-chained kernels each); the step-finish kernel of the body's last step
+// re-arms the loop while the run is RUNNING and fewer than loop_iters bodies of
+// this launch have run (hb_mm4.cu k_step_finish).  A run therefore stops within
+// the body of its stop step: at most chunk - 1 no-op steps, each a CTA launch
+// per stage that exits on the status (k_mm4), instead of whole graphs of them.
+// Kernels that cannot re-arm the loop (the generic k_stage) get a plain graph of
+// `chunk` steps per launch.
+static cudaError_t capture_steps(hb_handle* h, int n_steps, bool set_cond,
+                                 cudaGraphConditionalHandle cond) {
+  cudaError_t err = cudaSuccess;
+  for (int c = 0; c < n_steps && !err; ++c)
+    for (int s = 1; s <= 4 && !err; ++s) {
+      KParams p = stage_params(h, s);
+      if (set_cond && s == 4 && c == n_steps - 1) {
+        p.set_cond = 1;
+        p.cond = (unsigned long long)cond;
+        p.loop_iters = h->loop_iters;
+      }
+      err = launch_stage(s, p, h->stream);
+    }
+  return err;
+}
+
+static int build_while_graph(hb_handle* h, cudaGraphExec_t* exec, int64_t* nodes) {
+  cudaGraph_t g = nullptr;
+  CK(cudaGraphCreate(&g, 0));
+  struct GD { cudaGraph_t g; ~GD() { if (g) cudaGraphDestroy(g); } } gd{g};
+  cudaGraphConditionalHandle cond;
+  CK(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = cond;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  cudaError_t err = capture_steps(h, h->chunk, true, cond);
+  cudaGraph_t out = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(h->stream, &out);
+  if (err) return cuda_fail(err, "capture stage kernels");
+  if (e2) return cuda_fail(e2, "cudaStreamEndCapture");
+  *nodes = (int64_t)5 * h->chunk;
+  CK(cudaGraphInstantiate(exec, g, 0));
+  return HB_OK;
+}
+
+static int build_plain_graph(hb_handle* h, cudaGraphExec_t* exec, int64_t* nodes) {
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t err = capture_steps(h, h->chunk, false, 0);
+  cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
+  if (err) return cuda_fail(err, "capture stage kernels");
+  if (e2) return cuda_fail(e2, "cudaStreamEndCapture");
+  size_t n = 0;
+  err = cudaGraphGetNodes(g, nullptr, &n);
+  if (!err) err = cudaGraphInstantiate(exec, g, 0);
+  cudaGraphDestroy(g);
+  if (err) return cuda_fail(err, "cudaGraphInstantiate");
+  *nodes = (int64_t)n;
   return HB_OK;
 }
 
 static int ensure_graph(hb_handle* h) {
   if (h->graph && h->graph_layout == h->layout) return HB_OK;
   graph_cache_put(h);
+  h->graph_while = h->base.fast != 0;
   std::string key(reinterpret_cast<const char*>(&h->device), sizeof(int));
   key.append(reinterpret_cast<const char*>(&h->chunk), sizeof(int));
+  key.append(reinterpret_cast<const char*>(&h->loop_iters), sizeof(h->loop_iters));
+  key.append(1, h->graph_while ? 'w' : 'p');
   for (int s = 1; s <= 4; ++s) {
     const KParams p = stage_params(h, s);
     key.append(reinterpret_cast<const char*>(&p), sizeof(KParams));
@@ -816,26 +1019,27 @@ static int ensure_graph(hb_handle* h) {
     h->graph_layout = h->layout;
     return HB_OK;
   }
-  cudaGraph_t g;
-  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-  cudaError_t err = cudaSuccess;
-  for (int c = 0; c < h->chunk && !err; ++c)
-    for (int s = 1; s <= 4 && !err; ++s) err = launch_stage(s, stage_params(h, s), h->stream);
-  cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
-  if (err) return cuda_fail(err, "capture stage kernels");
-  if (e2) return cuda_fail(e2, "cudaStreamEndCapture");
-  size_t nodes = 0;
-  err = cudaGraphGetNodes(g, nullptr, &nodes);
-  if (err) {
-    cudaGraphDestroy(g);
-    return cuda_fail(err, "cudaGraphGetNodes");
+  int rc = h->graph_while ? build_while_graph(h, &h->graph, &h->graph_nodes)
+                          : build_plain_graph(h, &h->graph, &h->graph_nodes);
+  if (rc) {
+    h->graph = nullptr;
+    return rc;
   }
-  h->graph_nodes = (int64_t)nodes;
-  err = cudaGraphInstantiate(&h->graph, g, 0);
-  cudaGraphDestroy(g);
-  if (err) return cuda_fail(err, "cudaGraphInstantiate");
   h->graph_layout = h->layout;
   return HB_OK;
+}
+
+// smallest step s with s * dt >= t_end - 1e-9 (the t_end test of heom.py:359-361)
+static long long t_end_step(double t_end, double dt) {
+  long long s = (long long)std::floor((t_end - 1e-9) / dt) - 2;
+  if (s < 0) s = 0;
+  while ((double)s * dt < t_end - 1e-9) ++s;
+  return s;
+}
+
+// steps one graph launch covers at most (the record buffer holds a sync's worth)
+static int64_t launch_steps(const hb_handle* h) {
+  return h->graph_while ? h->loop_iters * h->chunk : h->chunk;
 }
 
 int hb_run(hb_handle* h, hb_result* res) {
@@ -843,11 +1047,14 @@ int hb_run(hb_handle* h, hb_result* res) {
   CK(cudaSetDevice(h->device));
   int rc = ensure_graph(h);
   if (rc) return rc;
+  const long long stop = h->prm.has_t_end ? t_end_step(h->prm.t_end, h->prm.dt) : -1;
   while (h->ctl_host->status == ST_RUNNING) {
-    // kGraphsPerSync chunks back to back: the device never idles while the host
-    // drains records and relaunches; a chunk enqueued after the stop early-exits
-    for (int g = 0; g < kGraphsPerSync; ++g) CK(cudaGraphLaunch(h->graph, h->stream));
-    h->launches += (int64_t)h->graph_nodes * kGraphsPerSync;
+    // kGraphsPerSync launches back to back: the device never idles while the host
+    // drains records and relaunches; a launch past the stop is a no-op body.  A
+    // t_end run that one launch finishes gets exactly one.
+    int n = kGraphsPerSync;
+    if (stop >= 0 && stop - h->ctl_host->step <= launch_steps(h)) n = 1;
+    for (int g = 0; g < n; ++g) CK(cudaGraphLaunch(h->graph, h->stream));
     rc = sync_ctl(h);
     if (rc) return rc;
     rc = drain(h);
@@ -943,6 +1150,10 @@ int hb_get_sigma0(hb_handle* h, double* sig0, double* sink_pops) {
 int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
   if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
   if (h->ctl_host->status != ST_RUNNING) return fail(HB_ERR_ARG, "run already stopped");
+  if (n_steps < 0) return fail(HB_ERR_ARG, "negative step count");
+  // the records of the timed steps stay on the device until the next sync
+  if (n_steps / h->prm.record_stride + 1 >= h->rec_cap)
+    return fail(HB_ERR_ARG, "record_stride too small for the timed step count (records would be dropped)");
   CK(cudaSetDevice(h->device));
   int rc = ensure_graph(h);
   if (rc) return rc;
@@ -952,23 +1163,21 @@ int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
   struct EG { cudaEvent_t a, b; ~EG() { cudaEventDestroy(a); cudaEventDestroy(b); } } eg{e0, e1};
   CK(cudaEventRecord(e0, h->stream));
   int64_t left = n_steps;
-  while (left >= h->chunk) {
+  const int64_t per_launch = launch_steps(h);
+  while (left >= per_launch) {
     CK(cudaGraphLaunch(h->graph, h->stream));
-    h->launches += h->graph_nodes;
-    left -= h->chunk;
+    left -= per_launch;
   }
-  const int64_t per_step = h->graph_nodes / h->chunk;  // kernels per RK4 step
-  for (; left > 0; --left) {
+  for (; left > 0; --left)
     for (int s = 1; s <= 4; ++s) CK(launch_stage(s, stage_params(h, s), h->stream));
-    h->launches += per_step;
-  }
   CK(cudaEventRecord(e1, h->stream));
   CK(cudaEventSynchronize(e1));
   float f = 0.f;
   CK(cudaEventElapsedTime(&f, e0, e1));
   *ms = f;
   if (stage_ms) {
-    // per-stage kernel durations: events around individual launches
+    // per-stage kernel durations: events around individual launches (these
+    // break the PDL overlap between stages, so they sum to more than a step)
     const int reps = 8;
     std::vector<cudaEvent_t> ev(reps * 5);
     for (auto& x : ev) CK(cudaEventCreate(&x));
@@ -978,7 +1187,6 @@ int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
         CK(launch_stage(s, stage_params(h, s), h->stream));
         CK(cudaEventRecord(ev[r * 5 + s], h->stream));
       }
-      h->launches += per_step;
     }
     CK(cudaEventSynchronize(ev.back()));
     for (int s = 0; s < 4; ++s) stage_ms[s] = 0.0;
@@ -999,7 +1207,11 @@ int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
   return HB_OK;
 }
 
-int64_t hb_launch_count(hb_handle* h) { return h ? h->launches : 0; }
+// kernels that did work: host-launched ones plus the step kernels the device
+// counted (current as of the handle's last synchronisation)
+int64_t hb_launch_count(hb_handle* h) {
+  return h ? h->launches + h->launches_base + (h->ctl_host ? h->ctl_host->launches : 0) : 0;
+}
 
 // ---------------------------------------------------------------------------
 // sharding
@@ -1009,7 +1221,6 @@ int hb_run_stage(hb_handle* h, int stage) {
   if (stage < 1 || stage > 4) return fail(HB_ERR_ARG, "stage must be 1..4");
   CK(cudaSetDevice(h->device));
   CK(launch_stage(stage, stage_params(h, stage), h->stream));
-  h->launches += 1;
   return HB_OK;
 }
 

@@ -1,4 +1,4 @@
-// Device-side helpers shared by the stage kernels (hb_stage.cu, hb_fast.cu):
+// Device-side helpers shared by the stage kernels (hb_stage.cu, hb_mm4.cu):
 // packed-plane bookkeeping, numpy-compatible summation and the scalar per-step
 // bookkeeping done by the last CTA of a stage-4 launch (sinks, guard, records,
 // stop policy -- heom.py:355-394).
@@ -103,37 +103,6 @@ __device__ __forceinline__ void load_sig0(const double* s, int i, int j, double&
     re = __ldcg(s + 2 * e * TILE);
     im = __ldcg(s + (2 * e + 1) * TILE);
   }
-}
-
-// TMA bulk prefetch of a contiguous range into L2 (no registers, no smem);
-// 16-byte aligned, size a multiple of 16
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// epilogue operands of a stage (sigma; + Y2, Y3 at stage 4) for one tile
-template <int STAGE>
-__device__ __forceinline__ void prefetch_epilogue(const KParams& P, size_t tile_off, unsigned bytes) {
-  if (STAGE >= 2) prefetch_l2(P.sig + tile_off, bytes);
-  if (STAGE == 4) {
-    prefetch_l2(P.Y2 + tile_off, bytes);
-    prefetch_l2(P.Y3 + tile_off, bytes);
-  }
-}
-
-// everything a stage reads for one tile except the gathers: own input, link
-// tables, epilogue operands -- bulk-prefetched into L2 one wave ahead
-template <int STAGE>
-__device__ __forceinline__ void prefetch_tile(const KParams& P, int tile) {
-  if (tile >= P.tile_begin + P.n_tiles) return;
-  const unsigned tbytes = (unsigned)(P.n_planes * TILE * sizeof(double));
-  const size_t off = (size_t)tile * P.n_planes * TILE;
-  prefetch_l2(P.Yin + off, tbytes);
-  prefetch_epilogue<STAGE>(P, off, tbytes);
-  const size_t goff = (size_t)tile * P.modes * TILE;
-  prefetch_l2(P.plus + goff, P.modes * TILE * 4);
-  prefetch_l2(P.minus + goff, P.modes * TILE * 4);
-  if ((P.modes * TILE) % 16 == 0) prefetch_l2(P.nvec + goff, P.modes * TILE);
 }
 
 // numpy add.reduce of a short float64 vector (pairwise_sum), see or_np_sum

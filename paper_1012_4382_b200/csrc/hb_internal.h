@@ -34,6 +34,7 @@ struct Ctl {
   unsigned int pad1;
   long long n_rec;                    // records in the device record buffer
   long long launches;                 // product-kernel launches that did work
+  long long loop_iter;                // WHILE-body iterations of the current graph launch
 };
 
 // Everything a stage kernel needs; passed by value (lives in the constant bank).
@@ -59,11 +60,14 @@ struct KParams {
   const int32_t* minus;
   const uint8_t* nvec;
   const double* damp_plane;  // optional per-ADO damping (Level-2 shim), else null
-  const double* zero_tile;   // NP*32 zeros: target of absent links (fast kernel)
-  int fast;                  // use the unrolled thread-per-ADO kernel (hb_fast.cu)
-  int prefetch;              // bulk-prefetch epilogue tiles into L2 at kernel start
-  int pf_dist;               // L2 prefetch distance in tiles (0 = off)
-  int debug;                 // timing experiments only (HB_DEBUG_NOGATHER): links -> zero tile
+  int fast;                  // production kernel k_mm4 (hb_mm4.cu), else the generic k_stage
+  int top_tile;              // first tile whose ADOs all sit on the top tier (no raise
+                             // links; tier-major order), n_tiles_total if none
+  const int32_t* tile_list;  // if set: block b computes tile tile_list[b] (sharded
+                             // boundary / interior launches), else tile_begin + b
+  int set_cond;              // k_step_finish of the last step of a WHILE-node body
+  long long loop_iters;      // WHILE-body iterations per graph launch
+  unsigned long long cond;   // cudaGraphConditionalHandle of that WHILE node
   int single;                // HB_PREC_SINGLE: the state buffers hold float (production
                              // kernel only); the operands below in float for its RHS
   float hf[MAXD * MAXD], decayf[MAXD], nuf[MAXKP1], af[MAXKP1], bf[MAXKP1];
@@ -94,21 +98,11 @@ struct KParams {
   double* rec_mats;
 };
 
-// hb_fast.cu: unrolled thread-per-ADO kernels for the production shape
-// (Hermitian layout, every block level is a site with site_of == identity)
-bool fast_supported(int d, int kp1);
-cudaError_t launch_fast(int stage, const KParams& p, cudaStream_t s);
-cudaError_t configure_fast(const KParams& p);  // before graph capture
-// hb_mm4.cu: production stage kernel (variant 7, default for d <= 8, K+1 <= 2)
+// hb_mm4.cu: production stage kernel for the Hermitian layout with every block
+// level a site (site_of == identity), d <= 8, K + 1 <= 2; stage 4 launches the
+// step bookkeeping kernel after it
+bool mm4_supported(int d, int kp1);
 cudaError_t launch_mm4(int stage, const KParams& p, cudaStream_t s);
-// hb_mm5.cu: link-slot-compacted stage kernel (variant 8)
-cudaError_t launch_mm5(int stage, const KParams& p, cudaStream_t s);
-// hb_mm6.cu: persistent contiguous-range stage kernel (variant 9)
-cudaError_t launch_mm6(int stage, const KParams& p, cudaStream_t s);
-// hb_mm8.cu: TMEM-accumulator stage kernel (variant 11, d = 7, K + 1 = 2)
-cudaError_t launch_mm8(int stage, const KParams& p, cudaStream_t s);
-// hb_mm9.cu: TMEM accumulator + pipelined gather rounds (variant 13, d = 7, K + 1 = 2)
-cudaError_t launch_mm9(int stage, const KParams& p, cudaStream_t s);
 
 // hb_stage.cu
 cudaError_t launch_stage(int stage, const KParams& p, cudaStream_t s);

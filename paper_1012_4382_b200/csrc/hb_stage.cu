@@ -271,7 +271,10 @@ __global__ void k_pack(const KParams P, const double* __restrict__ ref, const in
     plane_info<D, HERM>(p, i, j, part);
     v = ref[(k * D * D + i * D + j) * 2 + part];
   }
-  dst[idx] = v;
+  if (P.single)  // float state (HB_PREC_SINGLE): rounded once, like the reference's astype
+    reinterpret_cast<float*>(dst)[idx] = (float)v;
+  else
+    dst[idx] = v;
 }
 
 template <int D, bool HERM>
@@ -388,7 +391,7 @@ static cudaError_t dispatch_stage(int stage, const KParams& p, cudaStream_t s) {
   return cudaErrorInvalidValue;
 
 cudaError_t launch_stage(int stage, const KParams& p, cudaStream_t s) {
-  if (p.fast && stage >= 1) return launch_fast(stage, p, s);
+  if (p.fast && stage >= 1) return launch_mm4(stage, p, s);
   HB_DISPATCH_D(dispatch_stage, stage, p, s)
 }
 

@@ -1,4 +1,4 @@
-// Shared pieces of the unrolled production kernels (hb_fast.cu, hb_mm4.cu):
+// Shared pieces of the production kernel (hb_mm4.cu) and the halo kernels:
 // the Hermitian-packed plane map and the mbarrier / bulk-copy (TMA) helpers.
 #pragma once
 #include <cstdint>
@@ -64,19 +64,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// the same copy with an L2 evict-last policy (build-time experiment HB_TBL_KEEP:
-// the link tables, re-read every stage, kept in L2 against the streamed state)
-__device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, unsigned bytes,
-                                              uint64_t* bar) {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 

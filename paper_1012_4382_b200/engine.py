@@ -185,6 +185,12 @@ class DeviceRun:
         s = np.ascontiguousarray(list(sink_pops) or [0.0], dtype=np.float64)
         N.check(N.lib().hb_set_rho0(self._h, N.ptr(r), N.ptr(s)), "hb_set_rho0")
 
+    def set_state(self, sig: np.ndarray, sink_pops) -> None:
+        """Whole hierarchy state (n_tot, d, d) in the reference order (hb_set_state)."""
+        r = np.ascontiguousarray(sig, dtype=np.complex128)
+        s = np.ascontiguousarray(list(sink_pops) or [0.0], dtype=np.float64)
+        N.check(N.lib().hb_set_state(self._h, N.ptr(r), N.ptr(s)), "hb_set_state")
+
     def run(self) -> int:
         """Returns the C status (HB_OK / HB_DIVERGED / HB_HARDCAP); others raise."""
         res = N.HbResult()
