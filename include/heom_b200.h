@@ -215,6 +215,10 @@ int64_t hb_launch_count(hb_handle* h);
  * fails also trims the pool and retries).  Live handles are untouched. */
 void hb_pool_trim(void);
 
+/* Cumulative host->device and device->host bytes copied by the library since it
+ * was loaded (all handles and shims): the end-to-end benchmark's transfer count. */
+void hb_io_bytes(int64_t* h2d, int64_t* d2h);
+
 /* ---- Sharding (new, no reference counterpart) ----
  * A handle created with tile_begin/tile_count computes only that contiguous
  * range of tiles (device order); the handle owning tile 0 (the root, ADO 0)

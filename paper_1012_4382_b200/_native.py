@@ -27,7 +27,7 @@ HB_PREC = {"double": 0, "single": 1}
 #: every symbol include/heom_b200.h declares (checked by the CPU test-suite)
 EXPORTS = ("hb_last_error", "hb_device_count", "hb_hierarchy_size", "hb_graph_build",
            "hb_rhs", "hb_heom_rhs", "hb_add_scaled", "hb_rk4_update", "hb_max_abs2", "hb_create",
-           "hb_destroy", "hb_set_rho0", "hb_set_state", "hb_pool_trim", "hb_run", "hb_get_records", "hb_record_count", "hb_get_state",
+           "hb_destroy", "hb_set_rho0", "hb_set_state", "hb_pool_trim", "hb_io_bytes", "hb_run", "hb_get_records", "hb_record_count", "hb_get_state",
            "hb_get_sigma0", "hb_time_steps", "hb_launch_count", "hb_run_stage", "hb_sync",
            "hb_copy_tiles", "hb_nccl_unique_id", "hb_nccl_init", "hb_exchange",
            "hb_halo_set", "hb_halo_exchange", "hb_halo_pull")
@@ -91,6 +91,7 @@ def lib():
         "hb_set_rho0": (_i, [_p, _p, _p]),
         "hb_set_state": (_i, [_p, _p, _p]),
         "hb_pool_trim": (None, []),
+        "hb_io_bytes": (None, [C.POINTER(_i64), C.POINTER(_i64)]),
         "hb_run": (_i, [_p, C.POINTER(HbResult)]),
         "hb_get_records": (_i, [_p, _p, _p, _p, _i64]),
         "hb_record_count": (_i64, [_p]),
@@ -144,3 +145,10 @@ def check(rc: int, what: str = "") -> None:
 
 def ptr(a: np.ndarray) -> int:
     return a.ctypes.data
+
+
+def io_bytes():
+    """(host->device, device->host) bytes the library has copied so far."""
+    a, b = _i64(), _i64()
+    lib().hb_io_bytes(C.byref(a), C.byref(b))
+    return int(a.value), int(b.value)

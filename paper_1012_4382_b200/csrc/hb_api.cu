@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -37,6 +38,22 @@ static int cuda_fail(cudaError_t e, const char* where) {
     cudaError_t e_ = (x);                       \
     if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
   } while (0)
+
+// Host<->device bytes moved by the library (every copy goes through hb_memcpy):
+// the end-to-end benchmark reads them around a propagate() call.
+static std::atomic<long long> g_io_h2d{0}, g_io_d2h{0};
+
+static cudaError_t hb_memcpy(void* dst, const void* src, size_t n, cudaMemcpyKind kind,
+                             cudaStream_t s) {
+  if (kind == cudaMemcpyHostToDevice) g_io_h2d += (long long)n;
+  if (kind == cudaMemcpyDeviceToHost) g_io_d2h += (long long)n;
+  return cudaMemcpyAsync(dst, src, n, kind, s);
+}
+
+void hb_io_bytes(int64_t* h2d, int64_t* d2h) {
+  if (h2d) *h2d = g_io_h2d.load();
+  if (d2h) *d2h = g_io_d2h.load();
+}
 
 // Device hierarchy tables are immutable, so handles with the same
 // (modes, n_max, ordering, device) share one copy -- the analogue of the
@@ -251,8 +268,8 @@ static int rhs_impl(double* out, const double* sig, int64_t n_tot, int d, const 
   CK(dout.alloc(dev_bytes));
   CK(ddamp.alloc(n_pad * sizeof(double)));
   CK(cudaMemsetAsync(ddamp.p, 0, n_pad * sizeof(double), s));
-  CK(cudaMemcpyAsync(ddamp.p, tier_damp, (size_t)n_tot * sizeof(double), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(dref.p, sig, ref_bytes, cudaMemcpyHostToDevice, s));
+  CK(hb_memcpy(ddamp.p, tier_damp, (size_t)n_tot * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(hb_memcpy(dref.p, sig, ref_bytes, cudaMemcpyHostToDevice, s));
   CK(launch_pack(p, dref.as<double>(), gt.dev2ref, din.as<double>(), s));
   p.Yin = din.as<double>();
   p.Yout = dout.as<double>();
@@ -263,7 +280,7 @@ static int rhs_impl(double* out, const double* sig, int64_t n_tot, int d, const 
   CK(configure_stages(p));
   CK(launch_rhs_only(p, s));
   CK(launch_unpack(p, dout.as<double>(), gt.dev2ref, dref.as<double>(), s));
-  CK(cudaMemcpyAsync(out, dref.p, ref_bytes, cudaMemcpyDeviceToHost, s));
+  CK(hb_memcpy(out, dref.p, ref_bytes, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return HB_OK;
 }
@@ -298,18 +315,18 @@ static int elementwise(int op, double* out, const double* x, const double* y, co
   CK(o.alloc(bytes));
   CK(a.alloc(bytes));
   CK(b.alloc(bytes));
-  CK(cudaMemcpyAsync(a.p, x, bytes, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(b.p, y, bytes, cudaMemcpyHostToDevice, s));
+  CK(hb_memcpy(a.p, x, bytes, cudaMemcpyHostToDevice, s));
+  CK(hb_memcpy(b.p, y, bytes, cudaMemcpyHostToDevice, s));
   if (op == 1) {
     CK(cc.alloc(bytes));
     CK(dd.alloc(bytes));
-    CK(cudaMemcpyAsync(o.p, out, bytes, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(cc.p, z, bytes, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dd.p, w, bytes, cudaMemcpyHostToDevice, s));
+    CK(hb_memcpy(o.p, out, bytes, cudaMemcpyHostToDevice, s));
+    CK(hb_memcpy(cc.p, z, bytes, cudaMemcpyHostToDevice, s));
+    CK(hb_memcpy(dd.p, w, bytes, cudaMemcpyHostToDevice, s));
   }
   CK(launch_elementwise(op, n, o.as<double>(), a.as<double>(), b.as<double>(), cc.as<double>(),
                         dd.as<double>(), c, s));
-  CK(cudaMemcpyAsync(out, o.p, bytes, cudaMemcpyDeviceToHost, s));
+  CK(hb_memcpy(out, o.p, bytes, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return HB_OK;
 }
@@ -336,10 +353,10 @@ int hb_max_abs2(const double* x, int64_t n, double* result, int device) {
   CK(a.alloc(bytes));
   CK(r.alloc(sizeof(unsigned long long)));
   CK(cudaMemsetAsync(r.p, 0, sizeof(unsigned long long), s));
-  CK(cudaMemcpyAsync(a.p, x, bytes, cudaMemcpyHostToDevice, s));
+  CK(hb_memcpy(a.p, x, bytes, cudaMemcpyHostToDevice, s));
   CK(launch_max_abs2(n, a.as<double>(), r.as<unsigned long long>(), s));
   unsigned long long bits = 0;
-  CK(cudaMemcpyAsync(&bits, r.p, sizeof bits, cudaMemcpyDeviceToHost, s));
+  CK(hb_memcpy(&bits, r.p, sizeof bits, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   std::memcpy(result, &bits, sizeof(double));
   return HB_OK;
@@ -808,16 +825,16 @@ static int drain(hb_handle* h) {
   h->steps.resize(s0 + n);
   h->pops.resize((s0 + n) * df);
   std::vector<long long> st(n);
-  CK(cudaMemcpyAsync(st.data(), h->rec_step, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(h->pops.data() + s0 * df, h->rec_pops, n * df * sizeof(double),
+  CK(hb_memcpy(st.data(), h->rec_step, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  CK(hb_memcpy(h->pops.data() + s0 * df, h->rec_pops, n * df * sizeof(double),
                      cudaMemcpyDeviceToHost, h->stream));
   if (h->prm.record_matrices) {
     h->mats.resize((s0 + n) * df * df * 2);
-    CK(cudaMemcpyAsync(h->mats.data() + s0 * df * df * 2, h->rec_mats,
+    CK(hb_memcpy(h->mats.data() + s0 * df * df * 2, h->rec_mats,
                        n * df * df * 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   }
   const long long zero = 0;
-  CK(cudaMemcpyAsync(&h->ctl->n_rec, &zero, sizeof zero, cudaMemcpyHostToDevice, h->stream));
+  CK(hb_memcpy(&h->ctl->n_rec, &zero, sizeof zero, cudaMemcpyHostToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   for (long long i = 0; i < n; ++i) h->steps[s0 + i] = st[i];
   h->ctl_host->n_rec = 0;
@@ -825,7 +842,7 @@ static int drain(hb_handle* h) {
 }
 
 static int sync_ctl(hb_handle* h) {
-  CK(cudaMemcpyAsync(h->ctl_host, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+  CK(hb_memcpy(h->ctl_host, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return HB_OK;
 }
@@ -838,7 +855,7 @@ static int start_run(hb_handle* h, const double* sink_pops) {
   c.status = ST_RUNNING;
   for (int s = 0; s < h->prm.n_sinks; ++s) c.sink_pops[s] = sink_pops[s];
   std::memcpy(h->ctl_host, &c, sizeof c);
-  CK(cudaMemcpyAsync(h->ctl, h->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
+  CK(hb_memcpy(h->ctl, h->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
   h->steps.clear();
   h->pops.clear();
   h->mats.clear();
@@ -894,10 +911,10 @@ int hb_set_rho0(hb_handle* h, const double* rho0, const double* sink_pops) {
   }
   if (h->base.single) {  // pageable source: the copy is staged before the call returns
     std::vector<float> tile0f(tile0.begin(), tile0.end());
-    CK(cudaMemcpyAsync(h->buf[0], tile0f.data(), tile0f.size() * sizeof(float),
+    CK(hb_memcpy(h->buf[0], tile0f.data(), tile0f.size() * sizeof(float),
                        cudaMemcpyHostToDevice, h->stream));
   } else {
-    CK(cudaMemcpyAsync(h->buf[0], tile0.data(), tile0.size() * sizeof(double),
+    CK(hb_memcpy(h->buf[0], tile0.data(), tile0.size() * sizeof(double),
                        cudaMemcpyHostToDevice, h->stream));
   }
   return start_run(h, sink_pops);
@@ -929,7 +946,7 @@ int hb_set_state(hb_handle* h, const double* sig, const double* sink_pops) {
   const size_t ref_bytes = (size_t)h->n_tot * d * d * 2 * sizeof(double);
   DevBuf tmp;
   CK(tmp.alloc(ref_bytes));
-  CK(cudaMemcpyAsync(tmp.p, sig, ref_bytes, cudaMemcpyHostToDevice, h->stream));
+  CK(hb_memcpy(tmp.p, sig, ref_bytes, cudaMemcpyHostToDevice, h->stream));
   CK(launch_pack(h->base, tmp.as<double>(), h->gt.dev2ref, h->buf[0], h->stream));
   h->launches += 1;
   return start_run(h, sink_pops);  // synchronises before tmp is freed
@@ -1100,7 +1117,7 @@ int hb_get_state(hb_handle* h, double* sig, double* sink_pops) {
     CK(tmp.alloc(ref_bytes));
     KParams p = h->base;
     CK(launch_unpack(p, h->buf[0], h->gt.dev2ref, tmp.as<double>(), h->stream));
-    CK(cudaMemcpyAsync(sig, tmp.p, ref_bytes, cudaMemcpyDeviceToHost, h->stream));
+    CK(hb_memcpy(sig, tmp.p, ref_bytes, cudaMemcpyDeviceToHost, h->stream));
   }
   int rc = sync_ctl(h);
   if (rc) return rc;
@@ -1116,10 +1133,10 @@ int hb_get_sigma0(hb_handle* h, double* sig0, double* sink_pops) {
   std::vector<double> tile0((size_t)h->n_planes * TILE);
   std::vector<float> tile0f(h->base.single ? tile0.size() : 0);
   if (h->base.single)
-    CK(cudaMemcpyAsync(tile0f.data(), h->buf[0], tile0f.size() * sizeof(float),
+    CK(hb_memcpy(tile0f.data(), h->buf[0], tile0f.size() * sizeof(float),
                        cudaMemcpyDeviceToHost, h->stream));
   else
-    CK(cudaMemcpyAsync(tile0.data(), h->buf[0], tile0.size() * sizeof(double),
+    CK(hb_memcpy(tile0.data(), h->buf[0], tile0.size() * sizeof(double),
                        cudaMemcpyDeviceToHost, h->stream));
   int rc = sync_ctl(h);
   if (rc) return rc;
@@ -1413,10 +1430,11 @@ int hb_halo_set(hb_handle* h, int n_seg, const int32_t* peer, const int32_t* is_
   CK(cudaMalloc(&H.planes, planes.size() * sizeof(int16_t)));
   CK(cudaMalloc(&H.packed, (size_t)std::max<int64_t>(total, 1) * nc * elem_size(h)));
   if (total) {
-    CK(cudaMemcpy(H.pos, pos, total * sizeof(int32_t), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(H.site, site, total * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(hb_memcpy(H.pos, pos, total * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+    CK(hb_memcpy(H.site, site, total * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   }
-  CK(cudaMemcpy(H.planes, planes.data(), planes.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+  CK(hb_memcpy(H.planes, planes.data(), planes.size() * sizeof(int16_t), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
   return HB_OK;
 }
 
