@@ -95,8 +95,6 @@ typedef struct {
     int ordering;             /* HB_ORDER_*                                       */
     int chunk_steps;          /* RK4 steps per CUDA-graph launch (0 = default)    */
     int kernel_variant;       /* HB_KERNEL_*                                      */
-    int tile_begin;           /* sharding: first tile (32 ADOs) this handle owns  */
-    int tile_count;           /* sharding: tiles owned (0 = all from tile_begin)  */
     int precision;            /* HB_PREC_*                                        */
 } hb_params;
 
@@ -219,40 +217,52 @@ void hb_pool_trim(void);
  * was loaded (all handles and shims): the end-to-end benchmark's transfer count. */
 void hb_io_bytes(int64_t* h2d, int64_t* d2h);
 
-/* ---- Sharding (new, no reference counterpart) ----
- * A handle created with tile_begin/tile_count computes only that contiguous
- * range of tiles (device order); the handle owning tile 0 (the root, ADO 0)
- * does the sink integration, records and the full stop policy.  Between stages
- * the caller moves halo tiles of the stage output buffer between shards:
- * buffer index 0 = sigma, 1 = Y2, 2 = Y3, 3 = Y4 (stage s writes buffer s % 4).
- * Sharded runs support the t_end stop policy. */
-int hb_run_stage(hb_handle* h, int stage);          /* enqueue one stage kernel (1..4) */
-int hb_sync(hb_handle* h, int* status, int64_t* step);  /* wait, drain records, read status */
-/* copy tiles [first, first+count) of buffer `buf` from src into dst (same or peer
- * device), ordered after everything enqueued on both handles so far */
-int hb_copy_tiles(hb_handle* dst, hb_handle* src, int buf, int first_tile, int n_tiles);
-/* NCCL halo exchange (libnccl loaded at run time); id = ncclUniqueId (128 bytes) */
+/* ---- Sharding (new, no reference counterpart: SPEC.md:277) ----
+ * One hierarchy split over several handles (one per GPU over NCCL, or several
+ * in one process on one GPU for verification).  A shard numbers its ADO slots
+ * locally: its owned ADOs first -- those below the top tier, then the top-tier
+ * ones in whole tiles (no raise links: k_mm4's paired gather rounds) -- then
+ * halo slots for the neighbours owned by other shards; the buffers hold only
+ * owned + halo slots.  The host side (shard.py) builds the local tables, the
+ * halo plan and four launch groups partitioning the owned tiles.  The shard
+ * whose slot 0 holds ADO 0 (the root) does sinks, records and the stop policy;
+ * sharded runs use the t_end policy. */
+typedef struct {
+    int n_local;            /* ADO slots (a multiple of 32): owned tiles, then halo   */
+    int own_tiles;          /* tiles [0, own_tiles) are computed by this shard         */
+    int top_tile;           /* first owned tile whose ADOs all sit on the top tier      */
+    int root;               /* local slot 0 holds ADO 0                                  */
+    const int32_t* plus;    /* (n_local, modes) local raise links, -1 = none            */
+    const int32_t* minus;   /* (n_local, modes) local lower links, -2 = none            */
+    const uint8_t* nvec;    /* (n_local, modes) n_m                                      */
+    const int32_t* groups;  /* owned tiles of the four launch groups, concatenated:      */
+    int group_count[4];     /* send-only, interior, send+halo, halo-only (a partition)  */
+} hb_shard_tables;
+int hb_create_shard(const hb_params* params, const hb_shard_tables* tables, hb_handle** out);
+/* wait for the handle's work, drain records, read the status / step */
+int hb_sync(hb_handle* h, int* status, int64_t* step);
+/* NCCL (libnccl loaded at run time); id = ncclUniqueId (128 bytes) */
 int hb_nccl_unique_id(char* id128);
 int hb_nccl_init(hb_handle* h, const char* id128, int nranks, int rank);
-/* grouped ncclSend/ncclRecv of tile runs of buffer `buf` on the handle's stream:
- * entry i sends (is_send[i] = 1) or receives tiles [first[i], first[i]+count[i])
- * to / from rank peer[i] */
-int hb_exchange(hb_handle* h, int buf, int n, const int32_t* peer, const int32_t* first,
-                const int32_t* count, const int32_t* is_send);
 /* Compressed halos: a consumer reads from a halo ADO only the cross of the site
  * it reaches it through (2d-1 Hermitian-packed planes, _kernels.py:41-57), so
- * the plan lists (device position, site) entries instead of tiles.  Segment i
- * has count[i] consecutive entries of pos/site, exchanged with rank peer[i]
- * (is_send[i] = 1: this handle owns them).  Needs hb_set_rho0 first and the
- * Hermitian production layout. */
+ * the plan lists (local slot, site) entries.  Segment i has count[i] consecutive
+ * entries of pos/site exchanged with shard peer[i]: is_send[i] = 1 packs them
+ * from this shard's owned slots, 0 unpacks them into its halo slots; owner and
+ * consumer list a segment's entries in the same order.  After hb_set_rho0. */
 int hb_halo_set(hb_handle* h, int n_seg, const int32_t* peer, const int32_t* is_send,
                 const int32_t* count, const int32_t* pos, const int32_t* site);
-/* pack the send segments of buffer `buf`, grouped ncclSend/ncclRecv, unpack the
- * receive segments -- all on the handle's stream */
-int hb_halo_exchange(hb_handle* h, int buf);
-/* in-process shards on one device: copy the crosses of receive segment `seg` of
- * dst's plan from src's buffer `buf` into dst's, stream-ordered on both */
-int hb_halo_pull(hb_handle* dst, hb_handle* src, int buf, int seg);
+/* Enqueue n_steps RK4 steps of this shard (NCCL): per stage the send-only and
+ * interior tiles, then -- once the halo of the stage input has arrived -- the
+ * send+halo tiles; the output crosses go out on a second stream (pack, grouped
+ * ncclSend/ncclRecv, unpack) while the halo-only tiles compute.  Every 25th
+ * step the divergence max is all-reduced (ncclAllReduce MAX) so all shards stop
+ * together (heom.py:386-389).  ms_or_null: CUDA-event time (synchronises). */
+int hb_shard_steps(hb_handle* h, int64_t n_steps, double* ms_or_null);
+/* The same for n in-process shards on one device, the exchange as device
+ * copies of the packed crosses, every stage serialised (the bit-exactness check
+ * of partition, local numbering and halo plan). */
+int hb_shard_steps_local(hb_handle** shards, int n, int64_t n_steps, double* ms_or_null);
 
 #ifdef __cplusplus
 }

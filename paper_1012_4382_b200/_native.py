@@ -28,9 +28,9 @@ HB_PREC = {"double": 0, "single": 1}
 EXPORTS = ("hb_last_error", "hb_device_count", "hb_hierarchy_size", "hb_graph_build",
            "hb_rhs", "hb_heom_rhs", "hb_add_scaled", "hb_rk4_update", "hb_max_abs2", "hb_create",
            "hb_destroy", "hb_set_rho0", "hb_set_state", "hb_pool_trim", "hb_io_bytes", "hb_run", "hb_get_records", "hb_record_count", "hb_get_state",
-           "hb_get_sigma0", "hb_time_steps", "hb_launch_count", "hb_run_stage", "hb_sync",
-           "hb_copy_tiles", "hb_nccl_unique_id", "hb_nccl_init", "hb_exchange",
-           "hb_halo_set", "hb_halo_exchange", "hb_halo_pull")
+           "hb_get_sigma0", "hb_time_steps", "hb_launch_count", "hb_create_shard", "hb_sync",
+           "hb_nccl_unique_id", "hb_nccl_init", "hb_halo_set", "hb_shard_steps",
+           "hb_shard_steps_local")
 
 
 class HbParams(C.Structure):
@@ -46,8 +46,14 @@ class HbParams(C.Structure):
         ("record_stride", C.c_int64), ("record_matrices", C.c_int),
         ("blowup_norm", C.c_double), ("device", C.c_int), ("layout", C.c_int),
         ("ordering", C.c_int), ("chunk_steps", C.c_int), ("kernel_variant", C.c_int),
-        ("tile_begin", C.c_int), ("tile_count", C.c_int), ("precision", C.c_int),
+        ("precision", C.c_int),
     ]
+
+
+class HbShardTables(C.Structure):
+    _fields_ = [("n_local", C.c_int), ("own_tiles", C.c_int), ("top_tile", C.c_int),
+                ("root", C.c_int), ("plus", C.c_void_p), ("minus", C.c_void_p),
+                ("nvec", C.c_void_p), ("groups", C.c_void_p), ("group_count", C.c_int * 4)]
 
 
 class HbResult(C.Structure):
@@ -99,15 +105,13 @@ def lib():
         "hb_get_sigma0": (_i, [_p, _p, _p]),
         "hb_time_steps": (_i, [_p, _i64, C.POINTER(_d), _p]),
         "hb_launch_count": (_i64, [_p]),
-        "hb_run_stage": (_i, [_p, _i]),
+        "hb_create_shard": (_i, [C.POINTER(HbParams), C.POINTER(HbShardTables), C.POINTER(_p)]),
         "hb_sync": (_i, [_p, C.POINTER(_i), C.POINTER(_i64)]),
-        "hb_copy_tiles": (_i, [_p, _p, _i, _i, _i]),
         "hb_nccl_unique_id": (_i, [C.c_char_p]),
         "hb_nccl_init": (_i, [_p, C.c_char_p, _i, _i]),
-        "hb_exchange": (_i, [_p, _i, _i, _p, _p, _p, _p]),
         "hb_halo_set": (_i, [_p, _i, _p, _p, _p, _p, _p]),
-        "hb_halo_exchange": (_i, [_p, _i]),
-        "hb_halo_pull": (_i, [_p, _p, _i, _i]),
+        "hb_shard_steps": (_i, [_p, _i64, C.POINTER(_d)]),
+        "hb_shard_steps_local": (_i, [C.POINTER(_p), _i, _i64, C.POINTER(_d)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -19,32 +19,27 @@
 #include <string>
 #include <tuple>
 #include <vector>
-#include "hb_internal.h"
+#include "hb_handle.h"
 
 using namespace hb;
 
 static thread_local std::string g_err;
 
-static int fail(int code, const std::string& msg) {
+int hb::fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
-static int cuda_fail(cudaError_t e, const char* where) {
+int hb::cuda_fail(cudaError_t e, const char* where) {
   cudaGetLastError();  // clear sticky-free errors
   return fail(HB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
-#define CK(x)                                   \
-  do {                                          \
-    cudaError_t e_ = (x);                       \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
-  } while (0)
 
 // Host<->device bytes moved by the library (every copy goes through hb_memcpy):
 // the end-to-end benchmark reads them around a propagate() call.
 static std::atomic<long long> g_io_h2d{0}, g_io_d2h{0};
 
-static cudaError_t hb_memcpy(void* dst, const void* src, size_t n, cudaMemcpyKind kind,
-                             cudaStream_t s) {
+cudaError_t hb::hb_memcpy(void* dst, const void* src, size_t n, cudaMemcpyKind kind,
+                           cudaStream_t s) {
   if (kind == cudaMemcpyHostToDevice) g_io_h2d += (long long)n;
   if (kind == cudaMemcpyDeviceToHost) g_io_d2h += (long long)n;
   return cudaMemcpyAsync(dst, src, n, kind, s);
@@ -60,10 +55,6 @@ void hb_io_bytes(int64_t* h2d, int64_t* d2h) {
 // reference's lru_cache'd _graph (heom.py:222-224).
 namespace {
 using GraphKey = std::tuple<int, int, int, int>;
-struct CachedGraph {
-  GraphTables gt;
-  ~CachedGraph() { free_graph(&gt); }
-};
 std::mutex g_graph_mu;
 std::map<GraphKey, std::shared_ptr<CachedGraph>> g_graphs;  // LRU of 8, like lru_cache(8)
 std::vector<GraphKey> g_graph_lru;
@@ -100,59 +91,6 @@ cudaError_t shared_graph(int modes, int n_max, int ordering, int device, cudaStr
   return cudaSuccess;
 }
 }  // namespace
-
-struct hb_handle {
-  hb_params prm{};
-  std::vector<double> h, decay, nu, a, b, sink_rate;
-  std::vector<int32_t> site_of, sink_nterms, sink_pos, site_pos, block_full, sink_full;
-  int device = 0;
-  int modes = 0, n_tot = 0, n_tiles = 0;
-  int chunk = 64;
-  cudaStream_t stream = nullptr;
-  std::shared_ptr<CachedGraph> graph_ref;  // shared device tables
-  GraphTables gt;                          // copy of graph_ref->gt (non-owning)
-  int layout = 0;  // HB_LAYOUT_HERMITIAN / GENERAL once allocated
-  int n_planes = 0;
-  double* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // sigma, Y2, Y3, Y4, B
-  size_t buf_bytes = 0;
-  Ctl* ctl = nullptr;
-  Ctl* ctl_host = nullptr;  // pinned
-  long long* rec_step = nullptr;
-  double* rec_pops = nullptr;
-  double* rec_mats = nullptr;
-  long long rec_cap = 0;
-  KParams base{};
-  cudaGraphExec_t graph = nullptr;
-  int graph_layout = -1;
-  std::string graph_key;  // GraphCache key of `graph`
-  int64_t graph_nodes = 0;  // kernel launches in one body (WHILE) / replay (plain) of `graph`
-  bool graph_while = false;  // `graph` is a WHILE node over a body of `chunk` steps
-  long long loop_iters = 1;  // WHILE-body iterations per graph launch
-  std::vector<int64_t> steps;
-  std::vector<double> pops, mats;
-  int64_t launches = 0;       // host-launched kernels (init, pack/unpack)
-  int64_t launches_base = 0;  // device-counted step kernels of earlier runs of the handle
-  bool ready = false;  // rho0 set
-  int own_begin = 0, own_count = 0;  // sharding: owned tile range
-  void* nccl_comm = nullptr;
-  // compressed halo plan (hb_halo_set): segments of (position, site) entries
-  struct Halo {
-    int nc = 0;                                    // planes per cross (2d - 1)
-    std::vector<int> peer, is_send, count, off;    // per segment; off in entries
-    int32_t* pos = nullptr;                        // device, all segments
-    int32_t* site = nullptr;
-    int16_t* planes = nullptr;                     // device, [site][nc] plane index
-    void* packed = nullptr;                        // device staging, [entry][nc]
-  } halo;
-};
-
-static void free_halo(hb_handle* h) {
-  cudaFree(h->halo.pos);
-  cudaFree(h->halo.site);
-  cudaFree(h->halo.planes);
-  cudaFree(h->halo.packed);
-  h->halo = hb_handle::Halo{};
-}
 
 // definitions take C linkage from the extern "C" declarations in heom_b200.h
 
@@ -399,7 +337,7 @@ static void pool_trim_device(int device) {
   }
 }
 
-static cudaError_t pool_alloc(int device, size_t bytes, void** out) {
+cudaError_t hb::pool_alloc(int device, size_t bytes, void** out) {
   {
     BufPool& P = buf_pool();
     std::lock_guard<std::mutex> lk(P.mu);
@@ -420,7 +358,7 @@ static cudaError_t pool_alloc(int device, size_t bytes, void** out) {
   return e;
 }
 
-static void pool_release(int device, size_t bytes, void* p) {
+void hb::pool_release(int device, size_t bytes, void* p) {
   BufPool& P = buf_pool();
   std::lock_guard<std::mutex> lk(P.mu);
   if (P.cached + bytes > kPoolCap) {
@@ -560,15 +498,13 @@ static void free_state(hb_handle* h) {
   h->graph_layout = -1;
 }
 
-static void nccl_destroy(void* comm);
 
 void hb_destroy(hb_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  if (h->nccl_comm) nccl_destroy(h->nccl_comm);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  free_shard(h);
   free_state(h);
-  free_halo(h);
   h->graph_ref.reset();
   if (h->ctl) pool_release(h->device, sizeof(Ctl), h->ctl);
   if (h->ctl_host) pinned_release(h->ctl_host);
@@ -581,7 +517,8 @@ void hb_destroy(hb_handle* h) {
   delete h;
 }
 
-int hb_create(const hb_params* P, hb_handle** out) {
+// T != null: a shard (hb_create_shard) with caller-built local tables
+static int create_impl(const hb_params* P, const hb_shard_tables* T, hb_handle** out) {
   *out = nullptr;
   if (!P) return fail(HB_ERR_ARG, "null params");
   const hb_params& q = *P;
@@ -605,6 +542,23 @@ int hb_create(const hb_params* P, hb_handle** out) {
   int64_t n_tot = 0;
   int rc = check_graph_args(modes, q.n_max, &n_tot);
   if (rc) return rc;
+  if (T) {
+    if (T->n_local < TILE || T->n_local % TILE != 0)
+      return fail(HB_ERR_ARG, "shard: n_local must be a positive multiple of 32");
+    if (T->own_tiles < 1 || T->own_tiles > T->n_local / TILE)
+      return fail(HB_ERR_ARG, "shard: own_tiles outside the local slots");
+    if (!q.has_t_end) return fail(HB_ERR_ARG, "sharded runs need the t_end stop policy");
+    int gsum = 0;
+    for (int g = 0; g < 4; ++g) {
+      if (T->group_count[g] < 0) return fail(HB_ERR_ARG, "shard: negative group size");
+      gsum += T->group_count[g];
+    }
+    if (gsum != T->own_tiles) return fail(HB_ERR_ARG, "shard: the groups must partition the owned tiles");
+    for (int i = 0; i < gsum; ++i)
+      if (T->groups[i] < 0 || T->groups[i] >= T->own_tiles)
+        return fail(HB_ERR_ARG, "shard: group tile outside the owned tiles");
+    n_tot = T->n_local;
+  }
 
   hb_handle* h = new hb_handle();
   h->prm = q;
@@ -646,19 +600,25 @@ int hb_create(const hb_params* P, hb_handle** out) {
   if (e) return bail(e, "cudaSetDevice");
   e = stream_acquire(h->device, &h->stream);
   if (e) return bail(e, "cudaStreamCreate");
-  e = shared_graph(modes, q.n_max, q.ordering, h->device, h->stream, &h->graph_ref);
-  if (e) return bail(e, "build_graph");
-  h->gt = h->graph_ref->gt;
-  h->n_tiles = h->gt.n_tiles;
-  h->own_begin = q.tile_begin;
-  h->own_count = q.tile_count > 0 ? q.tile_count : h->n_tiles - q.tile_begin;
-  if (q.tile_begin < 0 || h->own_count < 1 || h->own_begin + h->own_count > h->n_tiles) {
-    hb_destroy(h);
-    return fail(HB_ERR_ARG, "tile range outside the hierarchy");
-  }
-  if (h->own_begin != 0 && !q.has_t_end) {
-    hb_destroy(h);
-    return fail(HB_ERR_ARG, "sharded runs need the t_end stop policy");
+  if (T) {
+    std::vector<uint8_t> nv(T->nvec, T->nvec + (size_t)T->n_local * modes);
+    e = upload_tables(modes, T->n_local, T->plus, T->minus, nv.data(), h->stream, &h->own_gt);
+    if (e) return bail(e, "upload shard tables");
+    h->gt = h->own_gt;
+    h->n_tiles = h->gt.n_tiles;
+    h->own_tiles = T->own_tiles;
+    h->shard = true;
+    int rs = init_shard(h, T);
+    if (rs) {
+      hb_destroy(h);
+      return rs;
+    }
+  } else {
+    e = shared_graph(modes, q.n_max, q.ordering, h->device, h->stream, &h->graph_ref);
+    if (e) return bail(e, "build_graph");
+    h->gt = h->graph_ref->gt;
+    h->n_tiles = h->gt.n_tiles;
+    h->own_tiles = h->n_tiles;
   }
   // small per-handle buffers come from the pool too: a handle of the same shape
   // then gets the same pointers, hence byte-identical kernel parameters, and can
@@ -685,10 +645,10 @@ int hb_create(const hb_params* P, hb_handle** out) {
   p.kp1 = q.kp1;
   p.modes = modes;
   p.n_tot = h->n_tot;
-  p.n_tiles = h->own_count;
+  p.n_tiles = h->own_tiles;
   p.n_tiles_total = h->n_tiles;
-  p.tile_begin = h->own_begin;
-  p.root = h->own_begin == 0;
+  p.tile_begin = 0;
+  p.root = T ? T->root != 0 : 1;
   for (int i = 0; i < d; ++i) {
     for (int j = 0; j < d; ++j) p.h[i * MAXD + j] = h->h[i * d + j];
     p.decay[i] = h->decay[i];
@@ -718,7 +678,9 @@ int hb_create(const hb_params* P, hb_handle** out) {
   // tier-major order: the top tier (no raise links) is the last
   // C(N_max + M - 1, N_max) positions; tiles wholly inside it skip the raise table
   p.top_tile = h->n_tiles;
-  if (q.ordering == HB_ORDER_REFERENCE) {
+  if (T) {
+    p.top_tile = T->top_tile;
+  } else if (q.ordering == HB_ORDER_REFERENCE) {
     const int64_t top_count = hierarchy_size(modes - 1, q.n_max);  // |n| = N_max exactly
     const int64_t first_top = n_tot - top_count;
     p.top_tile = (int)((first_top + TILE - 1) / TILE);
@@ -756,7 +718,14 @@ int hb_create(const hb_params* P, hb_handle** out) {
   return HB_OK;
 }
 
-static KParams stage_params(hb_handle* h, int stage) {
+int hb_create(const hb_params* P, hb_handle** out) { return create_impl(P, nullptr, out); }
+
+int hb_create_shard(const hb_params* P, const hb_shard_tables* T, hb_handle** out) {
+  if (!T) return fail(HB_ERR_ARG, "null shard tables");
+  return create_impl(P, T, out);
+}
+
+KParams hb::stage_params(hb_handle* h, int stage) {
   KParams p;
   std::memcpy(&p, &h->base, sizeof p);  // byte-exact (padding too): GraphCache keys
   double* S = h->buf[0];
@@ -778,7 +747,7 @@ static KParams stage_params(hb_handle* h, int stage) {
 }
 
 // bytes per state element: float for HB_PREC_SINGLE, double otherwise
-static size_t elem_size(const hb_handle* h) { return h->base.single ? sizeof(float) : sizeof(double); }
+size_t hb::elem_size(const hb_handle* h) { return h->base.single ? sizeof(float) : sizeof(double); }
 
 static int alloc_state(hb_handle* h, int layout) {
   if (h->layout == layout && h->buf[0]) return HB_OK;
@@ -816,7 +785,7 @@ static int alloc_state(hb_handle* h, int layout) {
   return HB_OK;
 }
 
-static int drain(hb_handle* h) {
+int hb::drain(hb_handle* h) {
   // ctl_host is current (caller synchronised)
   const long long n = h->ctl_host->n_rec;
   if (n <= 0) return HB_OK;
@@ -841,7 +810,7 @@ static int drain(hb_handle* h) {
   return HB_OK;
 }
 
-static int sync_ctl(hb_handle* h) {
+int hb::sync_ctl(hb_handle* h) {
   CK(hb_memcpy(h->ctl_host, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return HB_OK;
@@ -851,6 +820,8 @@ static int sync_ctl(hb_handle* h) {
 // stop policy before the first step (heom.py:355-368)
 static int start_run(hb_handle* h, const double* sink_pops) {
   h->launches_base += h->ctl_host->launches;  // the device count restarts with the block
+  h->host_step = 0;
+  for (bool& b : h->packed_once) b = false;
   Ctl c{};
   c.status = ST_RUNNING;
   for (int s = 0; s < h->prm.n_sinks; ++s) c.sink_pops[s] = sink_pops[s];
@@ -873,6 +844,7 @@ static int start_run(hb_handle* h, const double* sink_pops) {
 int hb_set_rho0(hb_handle* h, const double* rho0, const double* sink_pops) {
   if (!h) return fail(HB_ERR_ARG, "null handle");
   CK(cudaSetDevice(h->device));
+  if (h->comm) CK(cudaStreamSynchronize(h->comm));  // no exchange in flight on the buffers
   const int d = h->prm.d;
   int layout = h->prm.layout;
   if (layout == HB_LAYOUT_AUTO) {
@@ -909,21 +881,22 @@ int hb_set_rho0(hb_handle* h, const double* rho0, const double* sink_pops) {
       tile0[(size_t)(2 * k + 1) * TILE] = rho0[2 * k + 1];
     }
   }
-  if (h->base.single) {  // pageable source: the copy is staged before the call returns
+  if (!h->base.root) {  // a shard without ADO 0: auxiliaries only, all zero
+  } else if (h->base.single) {  // pageable source: the copy is staged before the call returns
     std::vector<float> tile0f(tile0.begin(), tile0.end());
     CK(hb_memcpy(h->buf[0], tile0f.data(), tile0f.size() * sizeof(float),
-                       cudaMemcpyHostToDevice, h->stream));
+                 cudaMemcpyHostToDevice, h->stream));
   } else {
     CK(hb_memcpy(h->buf[0], tile0.data(), tile0.size() * sizeof(double),
-                       cudaMemcpyHostToDevice, h->stream));
+                 cudaMemcpyHostToDevice, h->stream));
   }
+  if (h->shard) h->halo_primed = false;
   return start_run(h, sink_pops);
 }
 
 int hb_set_state(hb_handle* h, const double* sig, const double* sink_pops) {
   if (!h) return fail(HB_ERR_ARG, "null handle");
-  if (h->own_begin != 0 || h->own_count != h->n_tiles)
-    return fail(HB_ERR_ARG, "hb_set_state needs an unsharded handle");
+  if (h->shard) return fail(HB_ERR_ARG, "hb_set_state needs an unsharded handle");
   CK(cudaSetDevice(h->device));
   const int d = h->prm.d;
   int layout = h->prm.layout;
@@ -1061,6 +1034,7 @@ static int64_t launch_steps(const hb_handle* h) {
 
 int hb_run(hb_handle* h, hb_result* res) {
   if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
+  if (h->shard) return fail(HB_ERR_ARG, "shard handles step with hb_shard_steps");
   CK(cudaSetDevice(h->device));
   int rc = ensure_graph(h);
   if (rc) return rc;
@@ -1166,6 +1140,7 @@ int hb_get_sigma0(hb_handle* h, double* sig0, double* sink_pops) {
 
 int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
   if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
+  if (h->shard) return fail(HB_ERR_ARG, "shard handles step with hb_shard_steps");
   if (h->ctl_host->status != ST_RUNNING) return fail(HB_ERR_ARG, "run already stopped");
   if (n_steps < 0) return fail(HB_ERR_ARG, "negative step count");
   // the records of the timed steps stay on the device until the next sync
@@ -1228,270 +1203,5 @@ int hb_time_steps(hb_handle* h, int64_t n_steps, double* ms, double* stage_ms) {
 // counted (current as of the handle's last synchronisation)
 int64_t hb_launch_count(hb_handle* h) {
   return h ? h->launches + h->launches_base + (h->ctl_host ? h->ctl_host->launches : 0) : 0;
-}
-
-// ---------------------------------------------------------------------------
-// sharding
-
-int hb_run_stage(hb_handle* h, int stage) {
-  if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
-  if (stage < 1 || stage > 4) return fail(HB_ERR_ARG, "stage must be 1..4");
-  CK(cudaSetDevice(h->device));
-  CK(launch_stage(stage, stage_params(h, stage), h->stream));
-  return HB_OK;
-}
-
-int hb_sync(hb_handle* h, int* status, int64_t* step) {
-  if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
-  CK(cudaSetDevice(h->device));
-  int rc = sync_ctl(h);
-  if (rc) return rc;
-  rc = drain(h);
-  if (rc) return rc;
-  if (status) *status = h->ctl_host->status;
-  if (step) *step = h->ctl_host->step;
-  return HB_OK;
-}
-
-int hb_copy_tiles(hb_handle* dst, hb_handle* src, int buf, int first_tile, int n_tiles) {
-  if (!dst || !src || !dst->ready || !src->ready) return fail(HB_ERR_ARG, "handles not ready");
-  if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
-  if (dst->n_planes != src->n_planes || dst->n_tiles != src->n_tiles ||
-      dst->base.single != src->base.single)
-    return fail(HB_ERR_ARG, "handles have different layouts");
-  if (first_tile < 0 || n_tiles < 0 || first_tile + n_tiles > dst->n_tiles)
-    return fail(HB_ERR_ARG, "tile range outside the hierarchy");
-  if (n_tiles == 0) return HB_OK;
-  const size_t tb = (size_t)TILE * dst->n_planes * elem_size(dst);
-  cudaEvent_t ev;
-  CK(cudaSetDevice(src->device));
-  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  CK(cudaEventRecord(ev, src->stream));
-  CK(cudaSetDevice(dst->device));
-  CK(cudaStreamWaitEvent(dst->stream, ev, 0));
-  CK(cudaMemcpyPeerAsync(reinterpret_cast<char*>(dst->buf[buf]) + first_tile * tb, dst->device,
-                         reinterpret_cast<const char*>(src->buf[buf]) + first_tile * tb,
-                         src->device, n_tiles * tb, dst->stream));
-  // the source must not overwrite the tiles before the copy has read them
-  cudaEvent_t done;
-  CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-  CK(cudaEventRecord(done, dst->stream));
-  CK(cudaSetDevice(src->device));
-  CK(cudaStreamWaitEvent(src->stream, done, 0));
-  cudaEventDestroy(ev);
-  cudaEventDestroy(done);
-  return HB_OK;
-}
-
-// NCCL, resolved at run time so the library loads without it
-namespace {
-struct NcclApi {
-  typedef int (*GetUniqueId)(void*);
-  typedef int (*CommInitRank)(void**, int, const char*, int);  // ncclUniqueId passed by value
-  typedef int (*SendRecv)(const void*, size_t, int, int, void*, cudaStream_t);
-  typedef int (*Group)();
-  typedef int (*CommDestroy)(void*);
-  typedef const char* (*ErrStr)(int);
-  GetUniqueId get_id = nullptr;
-  void* init_rank = nullptr;
-  SendRecv send = nullptr;
-  SendRecv recv = nullptr;
-  Group group_start = nullptr, group_end = nullptr;
-  CommDestroy destroy = nullptr;
-  ErrStr err = nullptr;
-  bool ok = false;
-};
-struct NcclUniqueId { char internal[128]; };
-typedef int (*CommInitRankById)(void**, int, NcclUniqueId, int);
-
-NcclApi& nccl() {
-  static NcclApi api = [] {
-    NcclApi a;
-    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!lib) return a;
-    a.get_id = (NcclApi::GetUniqueId)dlsym(lib, "ncclGetUniqueId");
-    a.init_rank = dlsym(lib, "ncclCommInitRank");
-    a.send = (NcclApi::SendRecv)dlsym(lib, "ncclSend");
-    a.recv = (NcclApi::SendRecv)dlsym(lib, "ncclRecv");
-    a.group_start = (NcclApi::Group)dlsym(lib, "ncclGroupStart");
-    a.group_end = (NcclApi::Group)dlsym(lib, "ncclGroupEnd");
-    a.destroy = (NcclApi::CommDestroy)dlsym(lib, "ncclCommDestroy");
-    a.err = (NcclApi::ErrStr)dlsym(lib, "ncclGetErrorString");
-    a.ok = a.get_id && a.init_rank && a.send && a.recv && a.group_start && a.group_end;
-    return a;
-  }();
-  return api;
-}
-
-int nccl_fail(int r, const char* where) {
-  const char* m = nccl().err ? nccl().err(r) : "nccl error";
-  return fail(HB_ERR_CUDA, std::string(where) + ": " + m);
-}
-}  // namespace
-
-static void nccl_destroy(void* comm) {
-  if (nccl().destroy) nccl().destroy(comm);
-}
-
-int hb_nccl_unique_id(char* id128) {
-  if (!nccl().ok) return fail(HB_ERR_CUDA, "libnccl.so.2 not found");
-  const int r = nccl().get_id(id128);
-  return r ? nccl_fail(r, "ncclGetUniqueId") : HB_OK;
-}
-
-int hb_nccl_init(hb_handle* h, const char* id128, int nranks, int rank) {
-  if (!h) return fail(HB_ERR_ARG, "null handle");
-  if (!nccl().ok) return fail(HB_ERR_CUDA, "libnccl.so.2 not found");
-  CK(cudaSetDevice(h->device));
-  NcclUniqueId id;
-  std::memcpy(id.internal, id128, sizeof id.internal);
-  void* comm = nullptr;
-  const int r = reinterpret_cast<CommInitRankById>(nccl().init_rank)(&comm, nranks, id, rank);
-  if (r) return nccl_fail(r, "ncclCommInitRank");
-  h->nccl_comm = comm;
-  return HB_OK;
-}
-
-int hb_exchange(hb_handle* h, int buf, int n, const int32_t* peer, const int32_t* first,
-                const int32_t* count, const int32_t* is_send) {
-  if (!h || !h->ready || !h->nccl_comm) return fail(HB_ERR_ARG, "handle without NCCL communicator");
-  if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
-  CK(cudaSetDevice(h->device));
-  const size_t tb = (size_t)TILE * h->n_planes * elem_size(h);
-  int r = nccl().group_start();
-  if (r) return nccl_fail(r, "ncclGroupStart");
-  for (int i = 0; i < n; ++i) {
-    if (first[i] < 0 || count[i] < 0 || first[i] + count[i] > h->n_tiles) {
-      nccl().group_end();
-      return fail(HB_ERR_ARG, "tile range outside the hierarchy");
-    }
-    char* p = reinterpret_cast<char*>(h->buf[buf]) + first[i] * tb;
-    const size_t bytes = count[i] * tb;
-    r = is_send[i] ? nccl().send(p, bytes, /*ncclInt8*/ 0, peer[i], h->nccl_comm, h->stream)
-                   : nccl().recv(p, bytes, /*ncclInt8*/ 0, peer[i], h->nccl_comm, h->stream);
-    if (r) {
-      nccl().group_end();
-      return nccl_fail(r, is_send[i] ? "ncclSend" : "ncclRecv");
-    }
-  }
-  r = nccl().group_end();
-  return r ? nccl_fail(r, "ncclGroupEnd") : HB_OK;
-}
-
-// ---- compressed halos (hb_halo.cu) ----
-
-int hb_halo_set(hb_handle* h, int n_seg, const int32_t* peer, const int32_t* is_send,
-                const int32_t* count, const int32_t* pos, const int32_t* site) {
-  if (!h || !h->ready) return fail(HB_ERR_ARG, "hb_set_rho0 must be called first");
-  if (!h->base.fast || h->layout != HB_LAYOUT_HERMITIAN)
-    return fail(HB_ERR_ARG, "compressed halos need the Hermitian production layout");
-  if (n_seg < 0) return fail(HB_ERR_ARG, "negative segment count");
-  CK(cudaSetDevice(h->device));
-  CK(cudaStreamSynchronize(h->stream));
-  free_halo(h);
-  const int d = h->prm.d, nc = 2 * d - 1;
-  auto& H = h->halo;
-  H.nc = nc;
-  int64_t total = 0;
-  for (int i = 0; i < n_seg; ++i) {
-    if (count[i] < 0) return fail(HB_ERR_ARG, "negative segment size");
-    H.peer.push_back(peer[i]);
-    H.is_send.push_back(is_send[i] != 0);
-    H.count.push_back(count[i]);
-    H.off.push_back((int)total);
-    total += count[i];
-  }
-  if (total > INT32_MAX / nc) return fail(HB_ERR_ARG, "halo plan too large");
-  for (int64_t e = 0; e < total; ++e) {
-    if (pos[e] < 0 || pos[e] >= h->n_tot) return fail(HB_ERR_ARG, "halo position outside the hierarchy");
-    if (site[e] < 0 || site[e] >= d) return fail(HB_ERR_ARG, "halo site outside the block");
-  }
-  // Hermitian-packed planes of the cross of block position s (row/column s)
-  std::vector<int16_t> planes((size_t)d * nc);
-  auto packed_off = [&](int a, int b) {  // a < b
-    int e = 0;
-    for (int r = 0; r < a; ++r) e += d - 1 - r;
-    return e + (b - a - 1);
-  };
-  for (int s = 0; s < d; ++s) {
-    int q = 0;
-    planes[(size_t)s * nc + q++] = (int16_t)s;
-    for (int o = 0; o < d; ++o) {
-      if (o == s) continue;
-      const int re = d + 2 * packed_off(s < o ? s : o, s < o ? o : s);
-      planes[(size_t)s * nc + q++] = (int16_t)re;
-      planes[(size_t)s * nc + q++] = (int16_t)(re + 1);
-    }
-  }
-  const size_t ib = (size_t)std::max<int64_t>(total, 1) * sizeof(int32_t);
-  CK(cudaMalloc(&H.pos, ib));
-  CK(cudaMalloc(&H.site, ib));
-  CK(cudaMalloc(&H.planes, planes.size() * sizeof(int16_t)));
-  CK(cudaMalloc(&H.packed, (size_t)std::max<int64_t>(total, 1) * nc * elem_size(h)));
-  if (total) {
-    CK(hb_memcpy(H.pos, pos, total * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
-    CK(hb_memcpy(H.site, site, total * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
-  }
-  CK(hb_memcpy(H.planes, planes.data(), planes.size() * sizeof(int16_t), cudaMemcpyHostToDevice, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  return HB_OK;
-}
-
-int hb_halo_exchange(hb_handle* h, int buf) {
-  if (!h || !h->ready || !h->nccl_comm) return fail(HB_ERR_ARG, "handle without NCCL communicator");
-  if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
-  CK(cudaSetDevice(h->device));
-  auto& H = h->halo;
-  const bool single = h->base.single;
-  const size_t eb = elem_size(h);
-  auto seg_ptr = [&](int i) { return static_cast<char*>(H.packed) + (size_t)H.off[i] * H.nc * eb; };
-  for (size_t i = 0; i < H.count.size(); ++i)  // pack every send segment
-    if (H.is_send[i])
-      CK(launch_halo(0, single, nullptr, h->buf[buf], H.count[i], H.pos + H.off[i],
-                     H.site + H.off[i], H.planes, H.nc, h->n_planes, seg_ptr((int)i), h->stream));
-  int r = nccl().group_start();
-  if (r) return nccl_fail(r, "ncclGroupStart");
-  for (size_t i = 0; i < H.count.size(); ++i) {
-    const size_t bytes = (size_t)H.count[i] * H.nc * eb;
-    r = H.is_send[i] ? nccl().send(seg_ptr((int)i), bytes, 0, H.peer[i], h->nccl_comm, h->stream)
-                     : nccl().recv(seg_ptr((int)i), bytes, 0, H.peer[i], h->nccl_comm, h->stream);
-    if (r) {
-      nccl().group_end();
-      return nccl_fail(r, H.is_send[i] ? "ncclSend" : "ncclRecv");
-    }
-  }
-  r = nccl().group_end();
-  if (r) return nccl_fail(r, "ncclGroupEnd");
-  for (size_t i = 0; i < H.count.size(); ++i)  // scatter every receive segment
-    if (!H.is_send[i])
-      CK(launch_halo(1, single, h->buf[buf], nullptr, H.count[i], H.pos + H.off[i],
-                     H.site + H.off[i], H.planes, H.nc, h->n_planes, seg_ptr((int)i), h->stream));
-  return HB_OK;
-}
-
-int hb_halo_pull(hb_handle* dst, hb_handle* src, int buf, int seg) {
-  if (!dst || !src || !dst->ready || !src->ready) return fail(HB_ERR_ARG, "handles not ready");
-  if (buf < 0 || buf > 3) return fail(HB_ERR_ARG, "buffer index must be 0..3");
-  if (dst->device != src->device) return fail(HB_ERR_ARG, "hb_halo_pull needs both shards on one device");
-  if (dst->n_planes != src->n_planes || dst->n_tiles != src->n_tiles ||
-      dst->base.single != src->base.single)
-    return fail(HB_ERR_ARG, "handles have different layouts");
-  auto& H = dst->halo;
-  if (seg < 0 || seg >= (int)H.count.size() || H.is_send[seg])
-    return fail(HB_ERR_ARG, "not a receive segment of the destination's halo plan");
-  CK(cudaSetDevice(dst->device));
-  cudaEvent_t ev;
-  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  CK(cudaEventRecord(ev, src->stream));
-  CK(cudaStreamWaitEvent(dst->stream, ev, 0));
-  CK(launch_halo(2, dst->base.single, dst->buf[buf], src->buf[buf], H.count[seg],
-                 H.pos + H.off[seg], H.site + H.off[seg], H.planes, H.nc, dst->n_planes, nullptr,
-                 dst->stream));
-  // the source must not overwrite the crosses before the copy has read them
-  CK(cudaEventRecord(ev, dst->stream));
-  CK(cudaStreamWaitEvent(src->stream, ev, 0));
-  CK(cudaEventDestroy(ev));
-  return HB_OK;
 }
 

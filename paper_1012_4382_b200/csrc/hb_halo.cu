@@ -10,7 +10,9 @@
 // stage per GPU at P = 8).
 //   pack   : owner, entries of one send segment -> contiguous [entry][plane]
 //   unpack : consumer, contiguous -> the same planes of its full-size buffer
-//   copy   : in-process shards on one device, owner buffer -> consumer buffer
+// Positions are shard-local slots: the owner packs from its owned slots, the
+// consumer unpacks into its halo slots (both list a segment's entries in the
+// same order).
 #include "hb_internal.h"
 
 namespace hb {
@@ -39,17 +41,31 @@ __global__ void k_halo_unpack(T* __restrict__ buf, int n, const int32_t* __restr
   buf[(size_t)(t >> 5) * n_planes * TILE + (size_t)p * TILE + (t & 31)] = in[idx];
 }
 
-template <class T>
-__global__ void k_halo_copy(T* __restrict__ dst, const T* __restrict__ src, int n,
-                            const int32_t* __restrict__ pos, const int32_t* __restrict__ site,
-                            const int16_t* __restrict__ planes, int nc, int n_planes) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)n * nc) return;
-  const int e = (int)(idx / nc), q = (int)(idx % nc);
-  const int t = pos[e];
-  const int p = planes[site[e] * nc + q];
-  const size_t a = (size_t)(t >> 5) * n_planes * TILE + (size_t)p * TILE + (t & 31);
-  dst[a] = src[a];
+// in-process shards: the divergence max over the shards' control blocks (the
+// bit patterns of non-negative doubles order like the doubles), written back to
+// every block so that each shard's step bookkeeping sees the global value
+struct GuardPtrs {
+  unsigned long long* p[64];
+  int n;
+};
+
+__global__ void k_guard_max(GuardPtrs g) {
+  if (threadIdx.x != 0) return;
+  unsigned long long m = 0;
+  for (int i = 0; i < g.n; ++i) {
+    const unsigned long long v = *(volatile unsigned long long*)g.p[i];
+    m = v > m ? v : m;
+  }
+  for (int i = 0; i < g.n; ++i) *(volatile unsigned long long*)g.p[i] = m;
+}
+
+cudaError_t launch_guard_max(unsigned long long* const* bits, int n, cudaStream_t s) {
+  if (n < 1 || n > 64) return cudaErrorInvalidValue;
+  GuardPtrs g{};
+  for (int i = 0; i < n; ++i) g.p[i] = bits[i];
+  g.n = n;
+  k_guard_max<<<1, 32, 0, s>>>(g);
+  return cudaGetLastError();
 }
 
 static unsigned blocks(int n, int nc) { return (unsigned)(((int64_t)n * nc + 255) / 256); }
@@ -63,12 +79,10 @@ cudaError_t launch_halo(int op, bool single, void* dst, const void* src, int n, 
     using T = float;
     if (op == 0) k_halo_pack<T><<<g, 256, 0, s>>>((const T*)src, n, pos, site, planes, nc, n_planes, (T*)packed);
     if (op == 1) k_halo_unpack<T><<<g, 256, 0, s>>>((T*)dst, n, pos, site, planes, nc, n_planes, (const T*)packed);
-    if (op == 2) k_halo_copy<T><<<g, 256, 0, s>>>((T*)dst, (const T*)src, n, pos, site, planes, nc, n_planes);
   } else {
     using T = double;
     if (op == 0) k_halo_pack<T><<<g, 256, 0, s>>>((const T*)src, n, pos, site, planes, nc, n_planes, (T*)packed);
     if (op == 1) k_halo_unpack<T><<<g, 256, 0, s>>>((T*)dst, n, pos, site, planes, nc, n_planes, (const T*)packed);
-    if (op == 2) k_halo_copy<T><<<g, 256, 0, s>>>((T*)dst, (const T*)src, n, pos, site, planes, nc, n_planes);
   }
   return cudaGetLastError();
 }

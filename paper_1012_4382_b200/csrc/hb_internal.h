@@ -103,6 +103,10 @@ struct KParams {
 // step bookkeeping kernel after it
 bool mm4_supported(int d, int kp1);
 cudaError_t launch_mm4(int stage, const KParams& p, cudaStream_t s);
+cudaError_t launch_mm4_only(int stage, const KParams& p, cudaStream_t s);  // no bookkeeping
+cudaError_t launch_step_finish(const KParams& p, cudaStream_t s);         // k_step_finish
+// hb_halo.cu: the divergence max of n shards' control blocks, written back to all
+cudaError_t launch_guard_max(unsigned long long* const* bits, int n, cudaStream_t s);
 
 // hb_stage.cu
 cudaError_t launch_stage(int stage, const KParams& p, cudaStream_t s);
@@ -120,7 +124,7 @@ cudaError_t launch_max_abs2(int64_t n, const double* x, unsigned long long* bits
                             cudaStream_t s);
 
 // hb_halo.cu: compressed (cross-only) halo exchange; op 0 = pack src -> packed,
-// 1 = unpack packed -> dst, 2 = copy src -> dst (same addresses)
+// 1 = unpack packed -> dst
 cudaError_t launch_halo(int op, bool single, void* dst, const void* src, int n, const int32_t* pos,
                         const int32_t* site, const int16_t* planes, int nc, int n_planes,
                         void* packed, cudaStream_t s);

@@ -164,6 +164,34 @@ static cudaError_t mm4_kp1(int stage, const KParams& p, cudaStream_t s) {
   return p.kp1 == 1 ? mm4_t<D, 1>(stage, p, s) : mm4_t<D, 2>(stage, p, s);
 }
 
+// the stage kernel alone (sharded runs launch a stage as several tile groups and
+// the step bookkeeping once after the last)
+template <int D, int KP1>
+static cudaError_t mm4_only_t(int stage, const KParams& p, cudaStream_t s) {
+  return p.single ? mm4_stage<float, D, KP1>(stage, p, s) : mm4_stage<double, D, KP1>(stage, p, s);
+}
+template <int D>
+static cudaError_t mm4_only_kp1(int stage, const KParams& p, cudaStream_t s) {
+  if (stage == 5) return finish_go<D>(p, s);
+  return p.kp1 == 1 ? mm4_only_t<D, 1>(stage, p, s) : mm4_only_t<D, 2>(stage, p, s);
+}
+
+cudaError_t launch_mm4_only(int stage, const KParams& p, cudaStream_t s) {
+  switch (p.d) {
+    case 1: return mm4_only_kp1<1>(stage, p, s);
+    case 2: return mm4_only_kp1<2>(stage, p, s);
+    case 3: return mm4_only_kp1<3>(stage, p, s);
+    case 4: return mm4_only_kp1<4>(stage, p, s);
+    case 5: return mm4_only_kp1<5>(stage, p, s);
+    case 6: return mm4_only_kp1<6>(stage, p, s);
+    case 7: return mm4_only_kp1<7>(stage, p, s);
+    case 8: return mm4_only_kp1<8>(stage, p, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_step_finish(const KParams& p, cudaStream_t s) { return launch_mm4_only(5, p, s); }
+
 bool mm4_supported(int d, int kp1) { return d >= 1 && d <= 8 && kp1 >= 1 && kp1 <= 2; }
 
 cudaError_t launch_mm4(int stage, const KParams& p, cudaStream_t s) {

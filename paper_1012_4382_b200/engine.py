@@ -113,7 +113,7 @@ class DeviceRun:
                  residual=None, hard_cap_fs: float = 200_000.0, record_stride: int = 1,
                  record_matrices: bool = False, blowup_norm: float = 1e6, device: int = 0,
                  layout: str = "auto", ordering: str = "reference", chunk_steps: int = 0,
-                 kernel: str = "auto", tile_range=None, precision: str = "double"):
+                 kernel: str = "auto", precision: str = "double", shard=None):
         N.require_device(device)
         if ops.d > 9:
             raise ValueError("block dimension above 9 is not supported by the device kernels")
@@ -155,11 +155,25 @@ class DeviceRun:
         p.chunk_steps = int(chunk_steps)
         p.kernel_variant = N.HB_KERNEL[kernel]
         p.precision = N.HB_PREC[precision]
-        if tile_range is not None:  # sharding (shard.py): owned tiles [begin, begin + count)
-            p.tile_begin, p.tile_count = int(tile_range[0]), int(tile_range[1])
         self._params = p
         handle = C.c_void_p()
-        N.check(N.lib().hb_create(C.byref(p), C.byref(handle)), "hb_create")
+        if shard is None:
+            N.check(N.lib().hb_create(C.byref(p), C.byref(handle)), "hb_create")
+        else:  # one shard of a sharded run (shard.py ShardLayout): local tables
+            groups = np.ascontiguousarray(np.concatenate(shard.groups) if len(shard.groups) else
+                                          np.zeros(0), np.int32)
+            t = N.HbShardTables()
+            t.n_local, t.own_tiles, t.top_tile = shard.n_local, shard.own_tiles, shard.top_tile
+            t.root = int(shard.root)
+            keep.update(sp=np.ascontiguousarray(shard.plus, np.int32),
+                        sm=np.ascontiguousarray(shard.minus, np.int32),
+                        sn=np.ascontiguousarray(shard.nvec, np.uint8), sg=groups)
+            t.plus, t.minus = keep["sp"].ctypes.data, keep["sm"].ctypes.data
+            t.nvec, t.groups = keep["sn"].ctypes.data, keep["sg"].ctypes.data
+            for g in range(4):
+                t.group_count[g] = len(shard.groups[g])
+            N.check(N.lib().hb_create_shard(C.byref(p), C.byref(t), C.byref(handle)),
+                    "hb_create_shard")
         self._h = handle
         self.result = None
 

@@ -265,30 +265,37 @@ def test_dense_rk4_matches_reference_and_fast_path():
 
 # ------------------------------------------------- sharding (8(e)), one GPU
 
-@pytest.mark.parametrize("exchange", ["crosses", "tiles"])
-@pytest.mark.parametrize("n_shards,n_max", [(2, 3), (3, 3), (4, 5)])
-def test_sharded_run_is_bit_exact(n_shards, n_max, exchange):
+@pytest.mark.parametrize("n_shards,n_max,K", [(2, 3, 1), (3, 3, 1), (4, 5, 1), (8, 5, 1), (3, 6, 0)])
+def test_sharded_run_is_bit_exact(n_shards, n_max, K):
+    """ONE hierarchy split over in-process shards (local numbering, owned + halo
+    slots only, four launch groups, cross halos): every ADO of the final state,
+    the records and the sinks equal the unsharded run bit for bit."""
     from paper_1012_4382_b200.shard import ShardedRun
-    ops = BlockOperands(FMO, BATH300, RATES, 1)
+    ops = BlockOperands(FMO, BATH300, RATES, K)
     rho0 = np.zeros((7, 7), complex)
     rho0[0, 0] = 1.0
+    n_tot = xf.hierarchy_size(7 * (K + 1), n_max)
     with DeviceRun(ops, n_max, 1.0, t_end_fs=30.0, layout="hermitian") as ref:
         ref.set_rho0(rho0, [0.0, 0.0])
         assert ref.run() == N.HB_OK
         steps_ref, pops_ref, _ = ref.records()
         sig_ref, sinks_ref = ref.sigma0()
-    sr = ShardedRun(ops, n_max, 1.0, 30.0, n_shards, exchange=exchange)
+        state_ref, _ = ref.state(n_tot)
+    sr = ShardedRun(ops, n_max, 1.0, 30.0, n_shards)
     try:
-        assert sum(sr.plan.halo_tiles(q) for q in range(n_shards)) > 0
+        assert all(L.halo_entries() > 0 for L in sr.layouts)
+        assert sum(L.n_owned for L in sr.layouts) == n_tot
         sr.set_rho0(rho0, [0.0, 0.0])
         assert sr.run() == 1  # t_end
         steps, pops, _ = sr.records()
-        sig, sinks = sr.runs[0].sigma0()
+        sig, sinks = sr.sigma0()
+        state = sr.state(n_tot)
     finally:
         sr.close()
     assert np.array_equal(steps, steps_ref)
     assert np.array_equal(pops, pops_ref)          # bit-exact: same kernels, complete halos
     assert np.array_equal(sig, sig_ref) and np.array_equal(sinks, sinks_ref)
+    assert np.array_equal(state, state_ref)
 
 
 def test_sharded_single_precision_is_bit_exact():

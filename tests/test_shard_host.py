@@ -8,78 +8,93 @@ import numpy as np
 import pytest
 
 from oracle import oracle as orc
-from paper_1012_4382_b200.shard import (TILE, cross_halo_plan, device_tables_from_reference,
-                                        halo_plan, shard_ranges, stage_output_buffer)
+from paper_1012_4382_b200.shard import TILE, build_shards, shard_bounds, stage_output_buffer, t_end_steps
 
 
-def lex_perm(indices):
-    """device (pure lexicographic) position of every reference position"""
-    order = np.lexsort(indices.T[::-1])
-    perm = np.empty(len(order), np.int64)
-    perm[order] = np.arange(len(order))
-    return perm
+def _tables(modes, n_max):
+    ind, tiers, plus, minus = orc.enumerate_hierarchy(modes, n_max)
+    return ind, tiers, plus, minus
 
 
-def test_shard_ranges_cover_and_balance():
-    r = shard_ranges(9993, 8)
-    assert r[0][0] == 0 and sum(c for _, c in r) == 9993
-    assert all(r[i][0] + r[i][1] == r[i + 1][0] for i in range(7))
-    assert max(c for _, c in r) - min(c for _, c in r) <= 1
+def test_shard_bounds_cover_and_balance():
+    b = shard_bounds(319770, 8)
+    assert b[0] == 0 and b[-1] == 319770
+    assert np.max(np.diff(b)) - np.min(np.diff(b)) <= 1
     with pytest.raises(ValueError):
-        shard_ranges(3, 4)
+        shard_bounds(3, 4)
 
 
-@pytest.mark.parametrize("modes,n_max,shards", [(14, 3, 2), (14, 4, 5), (7, 6, 3)])
-def test_halo_plan_is_complete_and_minimal(modes, n_max, shards):
-    ind, _, plus, minus = orc.enumerate_hierarchy(modes, n_max)
-    perm = lex_perm(ind)
-    assert perm[0] == 0
-    pd, md = device_tables_from_reference(plus, minus, perm)
-    plan = halo_plan(pd, md, shards)
-    n_tiles = (len(ind) + TILE - 1) // TILE
-    for q, (b, c) in enumerate(plan.ranges):
-        have = set(range(b, b + c))
-        halo = set()
-        for owner, first, cnt in plan.recv[q]:
-            ob, oc = plan.ranges[owner]
-            assert ob <= first and first + cnt <= ob + oc
-            halo |= set(range(first, first + cnt))
-        lo, hi = b * TILE, min((b + c) * TILE, len(ind))
-        links = np.concatenate([pd[lo:hi].ravel(), md[lo:hi].ravel()])
-        need = set((links[links >= 0] // TILE).tolist())
-        assert need <= have | halo            # complete
-        assert halo <= need and not (halo & have)  # minimal
-        assert all(0 <= t < n_tiles for t in halo)
-    sends = sorted((o, q, f, c) for q in range(shards) for o, f, c in plan.recv[q])
-    assert sends == sorted((o, q, f, c) for o in range(shards) for q, f, c in plan.send[o])
-
-
-@pytest.mark.parametrize("modes,kp1,n_max,shards", [(14, 2, 3, 2), (14, 2, 4, 5), (7, 1, 6, 3)])
-def test_cross_halo_plan_is_complete_and_minimal(modes, kp1, n_max, shards):
-    ind, _, plus, minus = orc.enumerate_hierarchy(modes, n_max)
-    perm = lex_perm(ind)
-    pd, md = device_tables_from_reference(plus, minus, perm)
-    plan = cross_halo_plan(pd, md, shards, kp1, 7)
-    for q, (b, c) in enumerate(plan.ranges):
-        lo, hi = b * TILE, min((b + c) * TILE, len(ind))
+@pytest.mark.parametrize("modes,kp1,n_max,shards", [(14, 2, 3, 2), (14, 2, 4, 5), (7, 1, 6, 3),
+                                                    (14, 2, 5, 8)])
+def test_shard_layouts_are_consistent(modes, kp1, n_max, shards):
+    ind, tiers, plus, minus = _tables(modes, n_max)
+    n_tot = len(ind)
+    L = build_shards(ind, tiers, plus, minus, shards, kp1, n_max)
+    owned = np.concatenate([x.local2ref[: x.own_tiles * TILE] for x in L])
+    owned = owned[owned >= 0]
+    assert np.array_equal(np.sort(owned), np.arange(n_tot))          # a partition
+    assert sum(x.root for x in L) == 1 and L[0].root and L[0].local2ref[0] == 0
+    for x in L:
+        own_slots = x.own_tiles * TILE
+        assert x.n_local % TILE == 0 and x.n_local >= own_slots
+        slots = np.nonzero(x.local2ref[:own_slots] >= 0)[0]
+        ref = x.local2ref[slots]
+        # local links name the same ADOs as the reference links
+        for loc, glob, none in ((x.plus, plus, -1), (x.minus, minus, -2)):
+            lt, gt = loc[slots], glob[ref]
+            assert np.all((gt < 0) == (lt < 0)) and np.all(lt[gt < 0] == none)
+            assert np.array_equal(x.local2ref[lt[gt >= 0]], gt[gt >= 0])
+        assert np.array_equal(x.nvec[slots], ind[ref])
+        # whole top-tier tiles past top_tile, nothing of the top tier before it
+        top_ref = x.local2ref[x.top_tile * TILE:own_slots]
+        assert np.all(tiers[top_ref[top_ref >= 0]] == n_max)
+        assert np.all(tiers[x.local2ref[: x.top_tile * TILE][x.local2ref[: x.top_tile * TILE] >= 0]] < n_max)
+        # halo: exactly the (neighbour, site) pairs the owned ADOs reach elsewhere
         need = set()
         for m in range(modes):
-            for t in np.concatenate([pd[lo:hi, m], md[lo:hi, m]]):
-                if t >= 0 and not (b * TILE <= t < (b + c) * TILE):
-                    need.add((int(t), m // kp1))
+            for tab in (x.plus, x.minus):
+                t = tab[slots, m]
+                for v in t[t >= own_slots]:
+                    need.add((int(v), m // kp1))
         got = set()
-        for owner, pos, site in plan.recv[q]:
-            ob, oc = plan.ranges[owner]
-            assert np.all((pos >= ob * TILE) & (pos < (ob + oc) * TILE))
-            assert np.all(np.diff(pos.astype(np.int64) * 16 + site) > 0)   # sorted, unique
+        for o, pos, site in x.recv:
+            assert o != x.rank
+            assert np.all(pos >= own_slots)
             got |= set(zip(pos.tolist(), site.tolist()))
-        assert got == need                      # complete and minimal
-    pairs = sorted((o, q, len(p)) for q in range(shards) for o, p, _ in plan.recv[q])
-    assert pairs == sorted((o, q, len(p)) for o in range(shards) for q, p, _ in plan.send[o])
+        assert got == need
+        # the owner ships the same (ADO, site) entries in the same order
+        for o, pos, site in x.recv:
+            (c, spos, ssite), = [e for e in L[o].send if e[0] == x.rank]
+            assert np.array_equal(L[o].local2ref[spos], x.local2ref[pos])
+            assert np.array_equal(ssite, site) and np.all(spos < L[o].own_tiles * TILE)
+        # launch groups partition the owned tiles; halo readers are in groups 2, 3
+        g = np.concatenate(x.groups)
+        assert np.array_equal(np.sort(g), np.arange(x.own_tiles))
+        links = np.concatenate([x.plus[:own_slots], x.minus[:own_slots]], axis=1)
+        reads = np.any(links >= own_slots, axis=1).reshape(-1, TILE).any(axis=1)
+        assert np.all(reads[np.concatenate([x.groups[2], x.groups[3]])])
+        assert not np.any(reads[np.concatenate([x.groups[0], x.groups[1]])])
+        sends = np.zeros(x.own_tiles, bool)
+        for _, pos, _ in x.send:
+            sends[pos // TILE] = True
+        assert np.all(sends[np.concatenate([x.groups[0], x.groups[2]])])
+        assert not np.any(sends[np.concatenate([x.groups[1], x.groups[3]])])
 
 
-def test_stage_buffers():
+def test_halo_volume_config4():
+    """Config 4 (M = 14, N_max = 8) at P = 8: compressed crosses per stage per
+    shard and memory of owned + halo slots only."""
+    ind, tiers, plus, minus = _tables(14, 8)
+    L = build_shards(ind, tiers, plus, minus, 8, 2, 8)
+    assert max(x.halo_bytes_per_stage() for x in L) < 9e6
+    assert max(x.n_local for x in L) < 0.4 * len(ind)      # not the full hierarchy
+    assert all(x.top_tile < x.own_tiles for x in L)         # paired-round tiles on every shard
+
+
+def test_stage_buffers_and_steps():
     assert [stage_output_buffer(s) for s in (1, 2, 3, 4)] == [1, 2, 3, 0]
+    assert t_end_steps(1000.0, 1.0) == 1000 and t_end_steps(30.0, 1.0) == 30
+    assert t_end_steps(0.0, 2.5) == 0 and t_end_steps(10.0, 3.0) == 4
 
 
 def _free_port():
@@ -90,47 +105,11 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, out_q):
-    import torch
-    import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    import paper_1012_4382_b200 as xf
-    fmo = xf.build_fmo_system()
-    bath = xf.BathParams.from_timescale(35.0, 166.0, 300.0)
-    rates = xf.MarkovRates.from_inverse_ps(2.5, 250.0)
-    pb = orc.Problem(fmo, bath, rates, 3, 1)
-    perm = lex_perm(pb.indices)
-    pd, md = device_tables_from_reference(pb.plus, pb.minus, perm)
-    plan = halo_plan(pd, md, world)
-    rng = np.random.default_rng(11)
-    full = rng.standard_normal((pb.n_tot, 7, 7)) + 1j * rng.standard_normal((pb.n_tot, 7, 7))
-    n_pad = ((pb.n_tot + TILE - 1) // TILE) * TILE
-    dev = np.zeros((n_pad, 7, 7), complex)
-    dev[perm] = full                       # device-order copy of the global state
-    b, c = plan.ranges[rank]
-    local = np.zeros_like(dev)             # this rank knows only its own tiles ...
-    local[b * TILE:(b + c) * TILE] = dev[b * TILE:(b + c) * TILE]
-    # ... plus the halo it receives from the owners (the transport of hb_exchange)
-    reqs = []
-    for dst, first, cnt in plan.send[rank]:
-        t = torch.from_numpy(local[first * TILE:(first + cnt) * TILE].view(np.float64).copy())
-        reqs.append(dist.isend(t, dst))
-    for owner, first, cnt in plan.recv[rank]:
-        t = torch.empty((cnt * TILE, 7, 7 * 2), dtype=torch.float64)
-        dist.recv(t, owner)
-        local[first * TILE:(first + cnt) * TILE] = t.numpy().view(np.complex128)
-    for r in reqs:
-        r.wait()
-    rhs_local = pb.rhs(local[perm])        # oracle RHS on what this rank holds
-    rhs_full = pb.rhs(full)
-    mine = [k for k in range(pb.n_tot) if b * TILE <= perm[k] < (b + c) * TILE]
-    ok = np.array_equal(rhs_local[mine], rhs_full[mine])
-    out_q.put((rank, ok, len(mine), plan.halo_tiles(rank)))
-    dist.destroy_process_group()
-
-
 def _cross_worker(rank, world, port, out_q):
+    """One shard per process: its owned ADOs, NaN everywhere else; the crosses
+    its plan receives come from the owners over gloo (the transport of
+    hb_shard_steps); the oracle RHS on the LOCAL tables must equal the global
+    RHS on every owned ADO, bit for bit."""
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -140,67 +119,48 @@ def _cross_worker(rank, world, port, out_q):
     bath = xf.BathParams.from_timescale(35.0, 166.0, 300.0)
     rates = xf.MarkovRates.from_inverse_ps(2.5, 250.0)
     pb = orc.Problem(fmo, bath, rates, 3, 1)
-    perm = lex_perm(pb.indices)
-    pd, md = device_tables_from_reference(pb.plus, pb.minus, perm)
-    plan = cross_halo_plan(pd, md, world, 2, 7)
+    L = build_shards(pb.indices, pb.tiers, pb.plus, pb.minus, world, 2, 3)[rank]
     rng = np.random.default_rng(12)
     full = rng.standard_normal((pb.n_tot, 7, 7)) + 1j * rng.standard_normal((pb.n_tot, 7, 7))
     full = full + full.conj().transpose(0, 2, 1)          # Hermitian, like every ADO
-    n_pad = ((pb.n_tot + TILE - 1) // TILE) * TILE
-    dev = np.zeros((n_pad, 7, 7), complex)
-    dev[perm] = full
-    b, c = plan.ranges[rank]
-    local = np.full_like(dev, np.nan)      # everything this rank does not own: unknown
-    local[b * TILE:(b + c) * TILE] = dev[b * TILE:(b + c) * TILE]
+    own_slots = L.own_tiles * TILE
+    local = np.full((L.n_local, 7, 7), np.nan + 0j)
+    ok_own = L.local2ref[:own_slots] >= 0
+    local[:own_slots][ok_own] = full[L.local2ref[:own_slots][ok_own]]
 
     def cross(m, s):  # row and column s of each matrix: the 2d-1 shipped elements
-        return np.concatenate([m[:, s, :], m[:, :, s]], axis=1)
+        return np.concatenate([m[s, :], m[:, s]])
 
     reqs = []
-    for dst, pos, site in plan.send[rank]:
-        payload = np.stack([cross(local[pos[i]:pos[i] + 1], site[i])[0] for i in range(len(pos))])
+    for dst, pos, site in L.send:
+        payload = np.stack([cross(local[p], s) for p, s in zip(pos, site)])
         reqs.append(dist.isend(torch.from_numpy(payload.view(np.float64).copy()), dst))
-    for owner, pos, site in plan.recv[rank]:
-        t = torch.empty((len(pos), 14, 2), dtype=torch.float64)
+    for owner, pos, site in L.recv:
+        t = torch.empty((len(pos), 28), dtype=torch.float64)
         dist.recv(t, owner)
-        got = t.numpy().view(np.complex128)[..., 0]
-        for i in range(len(pos)):
-            local[pos[i], site[i], :] = got[i, :7]
-            local[pos[i], :, site[i]] = got[i, 7:]
+        got = t.numpy().view(np.complex128)
+        for i, (p, s) in enumerate(zip(pos, site)):
+            local[p, s, :] = got[i, :7]
+            local[p, :, s] = got[i, 7:]
     for r in reqs:
         r.wait()
-    rhs_local = pb.rhs(local[perm])
+    rhs_local = orc.rhs_from_arrays(local, pb.h, pb.site_of, L.plus, L.minus, L.nvec.astype(np.int32),
+                                    pb.n_sites, pb.kp1, pb.nu, pb.a, pb.b, pb.decay)
     rhs_full = pb.rhs(full)
-    mine = [k for k in range(pb.n_tot) if b * TILE <= perm[k] < (b + c) * TILE]
-    ok = np.array_equal(rhs_local[mine], rhs_full[mine])
-    out_q.put((rank, ok, len(mine), plan.entries(rank)))
+    slots = np.nonzero(ok_own)[0]
+    ok = np.array_equal(rhs_local[slots], rhs_full[L.local2ref[slots]])
+    out_q.put((rank, ok, len(slots), L.halo_entries()))
     dist.destroy_process_group()
 
 
 def test_gloo_cross_halo_exchange_reproduces_unsharded_rhs():
-    """only the crosses are shipped; the rest of every halo ADO is NaN here, so
+    """only the crosses are shipped; the rest of every halo slot is NaN here, so
     a kernel reading any other element of a neighbour would fail"""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_cross_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = sorted(q.get(timeout=240) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-    assert [r[1] for r in res] == [True, True]
-    assert sum(r[2] for r in res) == orc.hierarchy_size(14, 3)
-    assert all(r[3] > 0 for r in res)
-
-
-def test_gloo_halo_exchange_reproduces_unsharded_rhs():
-    import torch.multiprocessing as mp
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=240) for _ in procs)
