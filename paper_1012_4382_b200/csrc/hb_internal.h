@@ -65,6 +65,9 @@ struct KParams {
                              // links; tier-major order), n_tiles_total if none
   const int32_t* tile_list;  // if set: block b computes tile tile_list[b] (sharded
                              // boundary / interior launches), else tile_begin + b
+  long long apw_first_tile;  // L2 persisting window over tiles [first, first + n) of the
+  long long apw_tiles;       // stage input (0 tiles: none), hit ratio apw_hit
+  float apw_hit;
   int set_cond;              // k_step_finish of the last step of a WHILE-node body
   long long loop_iters;      // WHILE-body iterations per graph launch
   unsigned long long cond;   // cudaGraphConditionalHandle of that WHILE node

@@ -127,11 +127,23 @@ static cudaError_t mm4_go(const KParams& p, cudaStream_t s) {
   cfg.gridDim = dim3((unsigned)p.n_tiles);
   cfg.blockDim = dim3(32);
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  int n = 1;
+  if (p.apw_tiles > 0) {  // the gather targets of the stage input kept in L2
+    const size_t tb = (size_t)D * D * TILE * sizeof(T);
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr =
+        (void*)(reinterpret_cast<const char*>(p.Yin) + p.apw_first_tile * tb);
+    attr[1].val.accessPolicyWindow.num_bytes = (size_t)p.apw_tiles * tb;
+    attr[1].val.accessPolicyWindow.hitRatio = p.apw_hit;
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    n = 2;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, k_mm4<T, D, KP1, STAGE, CAP>, p);
 }
 
