@@ -433,20 +433,29 @@ static void pinned_release(Ctl* c) {
 // are untouched.
 void hb_pool_trim(void) { pool_trim_device(-1); }
 
-// The device's L2 set-aside for persisting accesses, set once per device to the
-// maximum (normal accesses use the set-aside while no persisting line holds it).
-static size_t persisting_l2(int device, size_t max_persist) {
+// The device's L2 set-aside for persisting accesses: grown to the largest
+// window a handle asked for (capped at the device maximum) -- a larger set-aside
+// than the window costs the streamed accesses L2 capacity (measured: the
+// 83 MB maximum against a 45 MB window makes config 4 17 % slower).
+static size_t persisting_l2(int device, size_t want, size_t max_persist) {
   static std::mutex mu;
-  static std::map<int, size_t> done;
+  static std::map<int, size_t> cur;
   std::lock_guard<std::mutex> lk(mu);
-  auto it = done.find(device);
-  if (it != done.end()) return it->second;
-  size_t got = 0;
-  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist) == cudaSuccess)
-    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
-  cudaGetLastError();
-  done[device] = got;
-  return got;
+  size_t& c = cur[device];
+  const size_t w = std::min(want, max_persist);
+  if (w > c) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, w) == cudaSuccess) {
+      size_t got = 0;
+      cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+      c = got;
+    }
+    cudaGetLastError();
+    cudaSetDevice(prev);
+  }
+  return c;
 }
 
 // Instantiated step graphs, keyed by the bytes of the four stages' kernel
@@ -691,6 +700,16 @@ static int create_impl(const hb_params* P, const hb_shard_tables* T, hb_handle**
   p.nvec = h->gt.nvec_t;
   p.damp_plane = nullptr;
   p.tile_list = nullptr;
+  // tier-major order: the top tier (no raise links) is the last
+  // C(N_max + M - 1, N_max) positions; tiles wholly inside it skip the raise table
+  p.top_tile = h->n_tiles;
+  if (T) {
+    p.top_tile = T->top_tile;
+  } else if (q.ordering == HB_ORDER_REFERENCE) {
+    const int64_t top_count = hierarchy_size(modes - 1, q.n_max);  // |n| = N_max exactly
+    const int64_t first_top = n_tot - top_count;
+    p.top_tile = (int)((first_top + TILE - 1) / TILE);
+  }
   // L2 persisting window over the stage input's tiers below N_max (tier-major
   // order: one contiguous prefix, 36 % of the ADOs at N_max = 8, K = 1): the
   // targets of the top tier's lower-link gathers stay in L2 while the state
@@ -710,7 +729,7 @@ static int create_impl(const hb_params* P, const hb_shard_tables* T, hb_handle**
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
     if (tiles > 0 && max_persist > 0 && buf_bytes > (size_t)l2 / 2) {
       const size_t want = (size_t)tiles * TILE * q.d * q.d * (q.precision == HB_PREC_SINGLE ? 4 : 8);
-      const size_t lim = persisting_l2(h->device, (size_t)max_persist);
+      const size_t lim = persisting_l2(h->device, want, (size_t)max_persist);
       if (lim > 0) {
         p.apw_first_tile = first;
         p.apw_tiles = tiles;
@@ -905,8 +924,8 @@ int hb_set_rho0(hb_handle* h, const double* rho0, const double* sink_pops) {
     for (int i = 0; i < d; ++i)
       for (int j = i + 1; j < d; ++j, ++e) {
         const int pr = d + 2 * (e - d);
-        tile0[(size_t)pr * TILE] = rho0[2 * (i * d + j)];
-        tile0[(size_t)(pr + 1) * TILE] = rho0[2 * (i * d + j) + 1];
+        tile0[herm_off(d, pr, 0)] = rho0[2 * (i * d + j)];
+        tile0[herm_off(d, pr + 1, 0)] = rho0[2 * (i * d + j) + 1];
       }
   } else {
     for (int k = 0; k < d * d; ++k) {
@@ -1148,7 +1167,8 @@ int hb_get_sigma0(hb_handle* h, double* sig0, double* sink_pops) {
   int rc = sync_ctl(h);
   if (rc) return rc;
   if (h->base.single) tile0.assign(tile0f.begin(), tile0f.end());
-  auto at = [&](int plane) { return tile0[(size_t)plane * TILE]; };  // lane 0 = ADO 0
+  const bool herm = h->layout == HB_LAYOUT_HERMITIAN;
+  auto at = [&](int plane) { return tile0[plane_off(herm, d, plane, 0)]; };  // lane 0 = ADO 0
   if (h->layout == HB_LAYOUT_HERMITIAN) {
     for (int i = 0; i < d; ++i) {
       sig0[2 * (i * d + i)] = at(i);

@@ -79,8 +79,8 @@ __device__ __forceinline__ void load_sig0(const double* s, int i, int j, double&
     for (int r = 0; r < a; ++r) e += D - 1 - r;
     e += b - a - 1;
     const int pr = D + 2 * (e - D);
-    re = (double)__ldcg(f + pr * TILE);
-    im = (double)__ldcg(f + (pr + 1) * TILE);
+    re = (double)__ldcg(f + herm_off(D, pr, 0));
+    im = (double)__ldcg(f + herm_off(D, pr + 1, 0));
     if (i > j) im = -im;
     return;
   }
@@ -95,8 +95,8 @@ __device__ __forceinline__ void load_sig0(const double* s, int i, int j, double&
     for (int r = 0; r < a; ++r) e += D - 1 - r;
     e += b - a - 1;
     const int pr = D + 2 * (e - D);
-    re = __ldcg(s + pr * TILE);
-    im = __ldcg(s + (pr + 1) * TILE);
+    re = __ldcg(s + herm_off(D, pr, 0));
+    im = __ldcg(s + herm_off(D, pr + 1, 0));
     if (i > j) im = -im;
   } else {
     const int e = i * D + j;

@@ -20,25 +20,25 @@ namespace hb {
 template <class T>
 __global__ void k_halo_pack(const T* __restrict__ buf, int n, const int32_t* __restrict__ pos,
                             const int32_t* __restrict__ site, const int16_t* __restrict__ planes,
-                            int nc, int n_planes, T* __restrict__ out) {
+                            int nc, int n_planes, int d, T* __restrict__ out) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * nc) return;
   const int e = (int)(idx / nc), q = (int)(idx % nc);
   const int t = pos[e];
   const int p = planes[site[e] * nc + q];
-  out[idx] = buf[(size_t)(t >> 5) * n_planes * TILE + (size_t)p * TILE + (t & 31)];
+  out[idx] = buf[(size_t)(t >> 5) * n_planes * TILE + herm_off(d, p, t & 31)];
 }
 
 template <class T>
 __global__ void k_halo_unpack(T* __restrict__ buf, int n, const int32_t* __restrict__ pos,
                               const int32_t* __restrict__ site, const int16_t* __restrict__ planes,
-                              int nc, int n_planes, const T* __restrict__ in) {
+                              int nc, int n_planes, int d, const T* __restrict__ in) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * nc) return;
   const int e = (int)(idx / nc), q = (int)(idx % nc);
   const int t = pos[e];
   const int p = planes[site[e] * nc + q];
-  buf[(size_t)(t >> 5) * n_planes * TILE + (size_t)p * TILE + (t & 31)] = in[idx];
+  buf[(size_t)(t >> 5) * n_planes * TILE + herm_off(d, p, t & 31)] = in[idx];
 }
 
 // in-process shards: the divergence max over the shards' control blocks (the
@@ -74,15 +74,16 @@ cudaError_t launch_halo(int op, bool single, void* dst, const void* src, int n, 
                         const int32_t* site, const int16_t* planes, int nc, int n_planes,
                         void* packed, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  const int d = (nc + 1) / 2;  // nc = 2d - 1 planes per cross (Hermitian layout)
   const unsigned g = blocks(n, nc);
   if (single) {
     using T = float;
-    if (op == 0) k_halo_pack<T><<<g, 256, 0, s>>>((const T*)src, n, pos, site, planes, nc, n_planes, (T*)packed);
-    if (op == 1) k_halo_unpack<T><<<g, 256, 0, s>>>((T*)dst, n, pos, site, planes, nc, n_planes, (const T*)packed);
+    if (op == 0) k_halo_pack<T><<<g, 256, 0, s>>>((const T*)src, n, pos, site, planes, nc, n_planes, d, (T*)packed);
+    if (op == 1) k_halo_unpack<T><<<g, 256, 0, s>>>((T*)dst, n, pos, site, planes, nc, n_planes, d, (const T*)packed);
   } else {
     using T = double;
-    if (op == 0) k_halo_pack<T><<<g, 256, 0, s>>>((const T*)src, n, pos, site, planes, nc, n_planes, (T*)packed);
-    if (op == 1) k_halo_unpack<T><<<g, 256, 0, s>>>((T*)dst, n, pos, site, planes, nc, n_planes, (const T*)packed);
+    if (op == 0) k_halo_pack<T><<<g, 256, 0, s>>>((const T*)src, n, pos, site, planes, nc, n_planes, d, (T*)packed);
+    if (op == 1) k_halo_unpack<T><<<g, 256, 0, s>>>((T*)dst, n, pos, site, planes, nc, n_planes, d, (const T*)packed);
   }
   return cudaGetLastError();
 }

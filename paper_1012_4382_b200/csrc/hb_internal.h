@@ -14,6 +14,20 @@ constexpr int MAXT = HB_MAX_SINK_TERMS;
 constexpr int MAX_MODES = 64;
 constexpr int MAXFULL = 16;       // full basis (block + sinks) for records
 
+// Hermitian-packed tile (HB_LAYOUT_HERMITIAN), 32 ADOs: the d real diagonal
+// planes [d][32], then the d(d-1)/2 upper-triangle elements as (re, im) pairs
+// [e][32][2], so a gathered complex element is one 16-byte load (8 for float).
+// Plane p < d is diagonal element p; plane d + 2e (+1) is the real (imaginary)
+// part of upper-triangle element e (row-major over i < j).  Returns the offset
+// of (plane p, lane) inside the tile, in elements.
+__host__ __device__ inline int herm_off(int d, int p, int lane) {
+  return p < d ? p * TILE + lane : d * TILE + ((p - d) >> 1) * 2 * TILE + 2 * lane + ((p - d) & 1);
+}
+// the generic (GENERAL) layout: plane-major [2 d^2][32]
+__host__ __device__ inline int plane_off(bool herm, int d, int p, int lane) {
+  return herm ? herm_off(d, p, lane) : p * TILE + lane;
+}
+
 enum Status : int {
   ST_RUNNING = 0,
   ST_T_END = 1,

@@ -31,8 +31,8 @@ __global__ void __launch_bounds__(32, CAP ? 12 : 1) k_mm4(const KParams P) {
   constexpr int M = D * KP1;
   constexpr int TB = NP * TILE;
   constexpr bool kInc = kIncScheme<T>;
-  __shared__ __align__(128) T sBase[STAGE >= 2 || kInc ? NP : 1][TILE];
-  __shared__ __align__(128) T sInc[kInc && (STAGE == 2 || STAGE == 4) ? NP : 1][TILE];
+  __shared__ __align__(128) T sBase[(STAGE >= 2 || kInc ? NP : 1) * TILE];
+  __shared__ __align__(128) T sInc[(kInc && (STAGE == 2 || STAGE == 4) ? NP : 1) * TILE];
   __shared__ __align__(16) int32_t sUp[M][TILE];
   __shared__ __align__(16) int32_t sDn[M][TILE];
   __shared__ __align__(16) uint8_t sN[M][TILE];
@@ -44,16 +44,16 @@ __global__ void __launch_bounds__(32, CAP ? 12 : 1) k_mm4(const KParams P) {
   if (ctl->status != ST_RUNNING) return;
   const int lane = threadIdx.x;
   const int tile = P.tile_list ? P.tile_list[blockIdx.x] : P.tile_begin + blockIdx.x;
-  const int own = tile * TB + lane;  // element offset of this lane's ADO, plane 0
+  const size_t tb = (size_t)tile * TB;  // element offset of the tile
   const T c = (T)(STAGE == 4 ? P.dt / 6.0 : P.coef);
   const bool top = tile >= P.top_tile;
 
   // operands no running kernel writes, before the grid dependency (PDL); the
   // float increment tile (written by stage 1) after it
-  tile_prologue<T, D, KP1, STAGE>(P, tile, &sBase[0][0], &sUp[0][0], &sDn[0][0], &sN[0][0],
-                                  &bar, !top, &sInc[0][0], true);
+  tile_prologue<T, D, KP1, STAGE>(P, tile, sBase, &sUp[0][0], &sDn[0][0], &sN[0][0], &bar, !top,
+                                  sInc, true);
   pdl_wait();
-  tile_prologue_late<T, D, STAGE>(P, tile, &sInc[0][0], &bar);
+  tile_prologue_late<T, D, STAGE>(P, tile, sInc, &bar);
   if (ctl->status != ST_RUNNING) {
     mbar_wait(&bar, 0);  // no bulk copy may land after the CTA has exited
     return;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(32, CAP ? 12 : 1) k_mm4(const KParams P) {
   pdl_release();
   const long long step_next = ctl->step + 1;
   T acc[NP];
-  phase_a<T, D, KP1, STAGE>(P, tile, lane, own, c, sBase, sN, &bar, acc);
+  phase_a<T, D, KP1, STAGE>(P, tile, lane, c, sBase, sN, &bar, acc);
   bool no_up = top;
   if (!top) {
     bool up_any = false;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(32, CAP ? 12 : 1) k_mm4(const KParams P) {
   }
   phase_b_sites<T, D, KP1>(P, lane, c, no_up, sUp, sDn, sN, acc);
   double maxa2 = 0.0;
-  phase_c_store<T, D, STAGE>(P, lane, own, sBase, acc, maxa2, sInc);
+  phase_c_store<T, D, STAGE>(P, lane, tb, sBase, acc, maxa2, sInc);
   if (STAGE == 4 && step_next % 25 == 0) {  // whole-state guard (heom.py:386-389)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxa2 = fmax(maxa2, __shfl_xor_sync(0xffffffffu, maxa2, o));

@@ -61,6 +61,24 @@ template <class T> __device__ __forceinline__ const T* st_sig(const KParams& P) 
 template <class T>
 constexpr bool kIncScheme = std::is_same<T, float>::value;
 
+// (re, im) pairs of the Hermitian tile layout (herm_off, hb_internal.h)
+template <class T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+template <class T> using v2_t = typename Vec2<T>::type;
+template <class T> __device__ __forceinline__ v2_t<T> ldg2(const T* p) {
+  return __ldg(reinterpret_cast<const v2_t<T>*>(p));
+}
+template <class T> __device__ __forceinline__ void st2(T* p, T x, T y) {
+  v2_t<T> v;
+  v.x = x;
+  v.y = y;
+  *reinterpret_cast<v2_t<T>*>(p) = v;
+}
+template <class T> __device__ __forceinline__ v2_t<T>& sm2(T* p) {
+  return *reinterpret_cast<v2_t<T>*>(p);
+}
+
 // load_up = false: the tile has no raise links (top tier), its raise table is
 // not copied
 template <class T, int D, int KP1, int STAGE>
@@ -112,16 +130,24 @@ __device__ __forceinline__ void pdl_release() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// phase A: acc = base + c (damping + commutator) with the ADO in registers
+// phase A: acc = base + c (damping + commutator) with the ADO in registers.
+// sBase: the tile's base operand (flat, Hermitian tile layout).
 template <class T, int D, int KP1, int STAGE>
-__device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, int own, T c,
-                                        T (*sBase)[TILE], const uint8_t (*sN)[TILE],
-                                        uint64_t* bar, T (&acc)[D * D]) {
-  constexpr int NP = D * D, M = D * KP1;
+__device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, T c, T* sBase,
+                                        const uint8_t (*sN)[TILE], uint64_t* bar,
+                                        T (&acc)[D * D]) {
+  constexpr int NP = D * D, M = D * KP1, DIAG = D * TILE, E = D * (D - 1) / 2;
   volatile Ctl* ctl = P.ctl;
+  const T* yo = st_in<T>(P) + (size_t)tile * NP * TILE;
   T s[NP];
 #pragma unroll
-  for (int p = 0; p < NP; ++p) s[p] = __ldg(st_in<T>(P) + own + p * TILE);
+  for (int i = 0; i < D; ++i) s[i] = __ldg(yo + i * TILE + lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const v2_t<T> v = ldg2(yo + DIAG + e * 2 * TILE + 2 * lane);
+    s[D + 2 * e] = v.x;
+    s[D + 2 * e + 1] = v.y;
+  }
   if (tile == 0 && lane == 0) {  // sink rates of this stage input (heom.py:282-283)
     int q = 0;
     for (int sk = 0; sk < P.n_sinks; ++sk) {
@@ -144,18 +170,7 @@ __device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, in
 #pragma unroll
   for (int k = 0; k < KP1; ++k) damp = fma((T)tk[k], Opd<T>::nu(P, k), damp);
   constexpr T third = (T)(1.0 / 3.0);
-  auto base = [&](int p) -> T {
-    if (kIncScheme<T>) {  // acc = increment; sigma kept (stage 1) or bulk-copied in sBase
-      if (STAGE == 1) sBase[p][lane] = s[p];
-      if (STAGE == 4) return (s[p] - sBase[p][lane]) * third;  // (Y4 - s)/3
-      return (T)0;
-    }
-    if (STAGE == 1) return s[p];
-    const T b = sBase[p][lane];
-    if (STAGE == 2) sBase[p][lane] = (s[p] - b) * third;  // park (Y2 - s)/3 for B
-    if (STAGE == 4) return fma(s[p], third, b);
-    return b;
-  };
+  constexpr bool kInc = kIncScheme<T>;
 #pragma unroll
   for (int i = 0; i < D; ++i) {
     // diagonal: Re(-i[H,s])_ii = 2 sum_{l != i} h_il Im s_il
@@ -164,10 +179,23 @@ __device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, in
     for (int l = 0; l < D; ++l)
       if (l != i) cm = fma(Opd<T>::h(P, i * MAXD + l), sim<T, D>(s, i, l), cm);
     const T fi = -(damp + Opd<T>::decay(P, i));
-    acc[i] = fma(c, fma(fi, s[i], (T)-2 * cm), base(i));
+    // the RK base term (see the header): sigma / B from shared memory
+    T* bs = sBase + i * TILE + lane;
+    T bv;
+    if constexpr (kInc) {
+      if (STAGE == 1) *bs = s[i];
+      bv = STAGE == 4 ? (s[i] - *bs) * third : (T)0;
+    } else if constexpr (STAGE == 1) {
+      bv = s[i];
+    } else {
+      const T b = *bs;
+      if (STAGE == 2) *bs = (s[i] - b) * third;  // park (Y2 - s)/3 for B
+      bv = STAGE == 4 ? fma(s[i], third, b) : b;
+    }
+    acc[i] = fma(c, fma(fi, s[i], (T)-2 * cm), bv);
 #pragma unroll
     for (int j = i + 1; j < D; ++j) {
-      const int pr = Pk<D>::re(i, j), pim = Pk<D>::im(i, j);
+      const int pr = Pk<D>::re(i, j), pim = Pk<D>::im(i, j), e = Pk<D>::off(i, j);
       // [H,s]_ij = sum_l h_il s_lj - s_il h_lj; the l = i and l = j terms pair up:
       // (h_ii - h_jj) s_ij + h_ij (s_jj - s_ii)  (s_ii, s_jj real)
       const T dh = Opd<T>::h(P, i * MAXD + i) - Opd<T>::h(P, j * MAXD + j);
@@ -184,24 +212,45 @@ __device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, in
         ci = fma(-hlj, sim<T, D>(s, i, l), ci);
       }
       const T f = -(damp + (T)0.5 * (Opd<T>::decay(P, i) + Opd<T>::decay(P, j)));
-      acc[pr] = fma(c, fma(f, s[pr], ci), base(pr));   // -1j * [H,s]
-      acc[pim] = fma(c, fma(f, s[pim], -cr), base(pim));
+      T* bp = sBase + DIAG + e * 2 * TILE + 2 * lane;
+      T br, bi;
+      if constexpr (kInc) {
+        if (STAGE == 1) st2(bp, s[pr], s[pim]);
+        if (STAGE == 4) {
+          const v2_t<T> b = sm2<T>(bp);
+          br = (s[pr] - b.x) * third;
+          bi = (s[pim] - b.y) * third;
+        } else {
+          br = bi = (T)0;
+        }
+      } else if constexpr (STAGE == 1) {
+        br = s[pr];
+        bi = s[pim];
+      } else {
+        const v2_t<T> b = sm2<T>(bp);
+        if (STAGE == 2) st2(bp, (s[pr] - b.x) * third, (s[pim] - b.y) * third);
+        br = STAGE == 4 ? fma(s[pr], third, b.x) : b.x;
+        bi = STAGE == 4 ? fma(s[pim], third, b.y) : b.y;
+      }
+      acc[pr] = fma(c, fma(f, s[pr], ci), br);   // -1j * [H,s]
+      acc[pim] = fma(c, fma(f, s[pim], -cr), bi);
     }
   }
 }
 
 // phase B: the neighbour crosses (_kernels.py:41-57), every term one FMA into the
 // register accumulator with the RK coefficient c folded into the link
-// coefficients (c n b_k, c n a_k, c); absent links are predicated off.
+// coefficients (c n b_k, c n a_k, c); absent links are predicated off.  Each
+// off-diagonal element of a cross is one (re, im) pair load.
 // no_up (warp-uniform): no lane of the tile has a raise link (the top tier) --
-// the lower links of GROUP sites are gathered per round trip (the same
-// 4(2d-1) loads as one full site), halving the dependent rounds of the tile.
+// the lower links of GROUP sites are gathered per round trip (the same loads as
+// one full site), halving the dependent rounds of the tile.
 template <class T, int D, int KP1, int GROUP = 2>
 __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c, bool no_up,
                                               const int32_t (*sUp)[TILE],
                                               const int32_t (*sDn)[TILE],
                                               const uint8_t (*sN)[TILE], T (&acc)[D * D]) {
-  constexpr int TB = D * D * TILE;
+  constexpr int TB = D * D * TILE, DIAG = D * TILE;
   const T* yin = st_in<T>(P);
   T cbk[KP1], cak[KP1];
 #pragma unroll
@@ -214,6 +263,15 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c, b
     if (v) r = __ldg(q);
     return r;
   };
+  auto ld2 = [](const T* q, bool v) -> v2_t<T> {
+    v2_t<T> r;
+    r.x = 0;
+    r.y = 0;
+    if (v) r = ldg2(q);
+    return r;
+  };
+  // link target t (position): its tile base and its lane
+  auto tbase = [&](int t) -> const T* { return yin + (size_t)(t >> 5) * TB; };
   if (no_up) {
 #pragma unroll
     for (int s0 = 0; s0 < D; s0 += GROUP) {
@@ -224,21 +282,23 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c, b
           const int m = st * KP1 + k;
           const int pd = sDn[m][lane];
           const bool vd = pd >= 0;
-          const T* dn = yin + ((pd >> 5) * TB + (pd & 31));
+          const T* dn = tbase(pd);
+          const int ld_ = pd & 31;
           const T n = vd ? (T)sN[m][lane] : (T)0;
           const T cb = n * cbk[k], ca = n * cak[k];
-          acc[st] = fma((T)2 * cb, ld(dn + st * TILE, vd), acc[st]);
+          acc[st] = fma((T)2 * cb, ld(dn + st * TILE + ld_, vd), acc[st]);
 #pragma unroll
           for (int o = 0; o < D; ++o) {
             if (o == st) continue;
             const int pr = Pk<D>::re(st, o), pim = Pk<D>::im(st, o);
-            const T dr = ld(dn + pr * TILE, vd), di = ld(dn + pim * TILE, vd);
+            const int e = Pk<D>::off(st < o ? st : o, st < o ? o : st);
+            const v2_t<T> dv = ld2(dn + DIAG + e * 2 * TILE + 2 * ld_, vd);
             if (o > st) {
-              acc[pr] = fma(cb, dr, fma(-ca, di, acc[pr]));
-              acc[pim] = fma(cb, di, fma(ca, dr, acc[pim]));
+              acc[pr] = fma(cb, dv.x, fma(-ca, dv.y, acc[pr]));
+              acc[pim] = fma(cb, dv.y, fma(ca, dv.x, acc[pim]));
             } else {
-              acc[pr] = fma(cb, dr, fma(ca, di, acc[pr]));
-              acc[pim] = fma(cb, di, fma(-ca, dr, acc[pim]));
+              acc[pr] = fma(cb, dv.x, fma(ca, dv.y, acc[pr]));
+              acc[pim] = fma(cb, dv.y, fma(-ca, dv.x, acc[pim]));
             }
           }
         }
@@ -253,24 +313,26 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c, b
       const int m = st * KP1 + k;
       const int pu = sUp[m][lane], pd = sDn[m][lane];
       const bool vu = pu >= 0, vd = pd >= 0;
-      const T* up = yin + ((pu >> 5) * TB + (pu & 31));
-      const T* dn = yin + ((pd >> 5) * TB + (pd & 31));
+      const T* up = tbase(pu);
+      const T* dn = tbase(pd);
+      const int lu = pu & 31, ld_ = pd & 31;
       const T n = vd ? (T)sN[m][lane] : (T)0;
       const T cb = n * cbk[k], ca = n * cak[k];
       const T cu = vu ? c : (T)0;
-      acc[st] = fma((T)2 * cb, ld(dn + st * TILE, vd), acc[st]);
+      acc[st] = fma((T)2 * cb, ld(dn + st * TILE + ld_, vd), acc[st]);
 #pragma unroll
       for (int o = 0; o < D; ++o) {
         if (o == st) continue;
         const int pr = Pk<D>::re(st, o), pim = Pk<D>::im(st, o);
-        const T ur = ld(up + pr * TILE, vu), ui = ld(up + pim * TILE, vu);
-        const T dr = ld(dn + pr * TILE, vd), di = ld(dn + pim * TILE, vd);
+        const int e = Pk<D>::off(st < o ? st : o, st < o ? o : st);
+        const v2_t<T> uv = ld2(up + DIAG + e * 2 * TILE + 2 * lu, vu);
+        const v2_t<T> dv = ld2(dn + DIAG + e * 2 * TILE + 2 * ld_, vd);
         if (o > st) {  // element (st, o): row st
-          acc[pr] = fma(cb, dr, fma(-ca, di, fma(-cu, ui, acc[pr])));
-          acc[pim] = fma(cb, di, fma(ca, dr, fma(cu, ur, acc[pim])));
+          acc[pr] = fma(cb, dv.x, fma(-ca, dv.y, fma(-cu, uv.y, acc[pr])));
+          acc[pim] = fma(cb, dv.y, fma(ca, dv.x, fma(cu, uv.x, acc[pim])));
         } else {       // element (o, st): column st
-          acc[pr] = fma(cb, dr, fma(ca, di, fma(cu, ui, acc[pr])));
-          acc[pim] = fma(cb, di, fma(-ca, dr, fma(-cu, ur, acc[pim])));
+          acc[pr] = fma(cb, dv.x, fma(ca, dv.y, fma(cu, uv.y, acc[pr])));
+          acc[pim] = fma(cb, dv.y, fma(-ca, dv.x, fma(-cu, uv.x, acc[pim])));
         }
       }
     }
@@ -278,35 +340,59 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c, b
 }
 
 // phase C: store (stage 2 also B = (Y2 - s)/3 + 2/3 Y3; float: see the header);
-// stage 4 also max|y|^2 over the lane's elements (diagonal planes are real)
+// stage 4 also max|y|^2 over the lane's elements (diagonal planes are real).
+// tb: element offset of the tile; sBase / sInc flat (Hermitian tile layout).
 template <class T, int D, int STAGE>
-__device__ __forceinline__ void phase_c_store(const KParams& P, int lane, int own,
-                                              T (*sBase)[TILE], T (&acc)[D * D],
-                                              double& maxa2, T (*sInc)[TILE] = nullptr) {
-  constexpr int NP = D * D;
+__device__ __forceinline__ void phase_c_store(const KParams& P, int lane, size_t tb, T* sBase,
+                                              T (&acc)[D * D], double& maxa2, T* sInc) {
+  constexpr int DIAG = D * TILE, E = D * (D - 1) / 2;
   constexpr T third = (T)(1.0 / 3.0), two3 = (T)(2.0 / 3.0);
-#pragma unroll
-  for (int p = 0; p < NP; ++p) {
+  T* out = st_out<T>(P) + tb;
+  T* bo = st_b<T>(P) + tb;
+  // one element: slot offset o (diagonal) -> value stored, B store as a side effect
+  auto fin = [&](T a, int o) -> T {
     if (kIncScheme<T>) {
-      const T a = acc[p], sg = sBase[p][lane];
-      if (STAGE == 1) st_b<T>(P)[own + p * TILE] = a * third;
-      if (STAGE == 2) st_b<T>(P)[own + p * TILE] = fma(two3, a, sInc[p][lane]);
-      acc[p] = STAGE == 4 ? sg + (sInc[p][lane] + a) : sg + a;
-      st_out<T>(P)[own + p * TILE] = acc[p];
-    } else {
-      st_out<T>(P)[own + p * TILE] = acc[p];
-      if (STAGE == 2) st_b<T>(P)[own + p * TILE] = fma(two3, acc[p], sBase[p][lane]);
+      const T sg = sBase[o];
+      if (STAGE == 1) bo[o] = a * third;
+      if (STAGE == 2) bo[o] = fma(two3, a, sInc[o]);
+      return STAGE == 4 ? sg + (sInc[o] + a) : sg + a;
     }
+    if (STAGE == 2) bo[o] = fma(two3, a, sBase[o]);
+    return a;
+  };
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    acc[i] = fin(acc[i], i * TILE + lane);
+    out[i * TILE + lane] = acc[i];
+  }
+  // the upper triangle, element e = planes D + 2e (re), D + 2e + 1 (im)
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int pr = D + 2 * e, pim = pr + 1;
+    const int o = DIAG + e * 2 * TILE + 2 * lane;
+    if (kIncScheme<T>) {
+      const v2_t<T> sg = sm2<T>(sBase + o);
+      v2_t<T> in;
+      in.x = 0;
+      in.y = 0;
+      if (STAGE == 2 || STAGE == 4) in = sm2<T>(sInc + o);
+      if (STAGE == 1) st2(bo + o, acc[pr] * third, acc[pim] * third);
+      if (STAGE == 2) st2(bo + o, fma(two3, acc[pr], in.x), fma(two3, acc[pim], in.y));
+      acc[pr] = STAGE == 4 ? sg.x + (in.x + acc[pr]) : sg.x + acc[pr];
+      acc[pim] = STAGE == 4 ? sg.y + (in.y + acc[pim]) : sg.y + acc[pim];
+    } else if (STAGE == 2) {
+      const v2_t<T> b = sm2<T>(sBase + o);
+      st2(bo + o, fma(two3, acc[pr], b.x), fma(two3, acc[pim], b.y));
+    }
+    st2(out + o, acc[pr], acc[pim]);
   }
   if (STAGE == 4) {
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      maxa2 = fmax(maxa2, (double)acc[i] * (double)acc[i]);
+    for (int i = 0; i < D; ++i) maxa2 = fmax(maxa2, (double)acc[i] * (double)acc[i]);
 #pragma unroll
-      for (int j = i + 1; j < D; ++j) {
-        const double yr = acc[Pk<D>::re(i, j)], yi = acc[Pk<D>::im(i, j)];
-        maxa2 = fmax(maxa2, fma(yr, yr, yi * yi));
-      }
+    for (int e = 0; e < E; ++e) {
+      const double yr = acc[D + 2 * e], yi = acc[D + 2 * e + 1];
+      maxa2 = fmax(maxa2, fma(yr, yr, yi * yi));
     }
   }
 }

@@ -35,6 +35,19 @@
 
 namespace hb {
 
+// tile slot idx (0 .. NP*32-1, in memory order) -> (plane, lane)
+template <int D, bool HERM>
+__device__ __forceinline__ void slot_info(int idx, int& p, int& l) {
+  if (!HERM || idx < D * TILE) {
+    p = idx >> 5;
+    l = idx & 31;
+    return;
+  }
+  const int r = idx - D * TILE;
+  p = D + 2 * (r >> 6) + (r & 1);
+  l = (r >> 1) & 31;
+}
+
 // ---------------------------------------------------------------------------
 // the stage kernel
 
@@ -63,7 +76,8 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
 
   const size_t tbase = (size_t)tile * NP * TILE;
   for (int idx = threadIdx.x; idx < NP * TILE; idx += D * 32) {
-    const int p = idx >> 5, l = idx & 31;
+    int p, l;
+    slot_info<D, HERM>(idx, p, l);
     const double v = __ldg(P.Yin + tbase + idx);
     int i, j, part;
     plane_info<D, HERM>(p, i, j, part);
@@ -117,7 +131,7 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
   }
 
   double maxa2 = 0.0;
-  const size_t obase = tbase + lane;
+  auto at = [&](int plane, int ln) -> int { return plane_off(HERM, D, plane, ln); };
   for (int e = warp; e < NE; e += D) {
     int i, j, pr, pim;
     elem_info<D, HERM>(e, i, j, pr, pim);
@@ -140,8 +154,8 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
         const int m = mi * P.kp1 + kk;
         const int p = s_plus[m * TILE + lane];
         if (!diag && p >= 0) {  // + 1j * sig[p][i,j]
-          const double* nb = P.Yin + (size_t)(p >> 5) * NP * TILE + (p & 31);
-          const double xr = __ldg(nb + pr * TILE), xi = __ldg(nb + pim * TILE);
+          const double* nb = P.Yin + (size_t)(p >> 5) * NP * TILE;
+          const double xr = __ldg(nb + at(pr, p & 31)), xi = __ldg(nb + at(pim, p & 31));
           ar -= xi;
           ai += xr;
         }
@@ -149,9 +163,9 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
         if (q >= 0) {  // + n (b + 1j a) sig[q][i,j]
           const double n = (double)s_nv[m * TILE + lane];
           const double cb = n * P.b[kk], ca = n * P.a[kk];
-          const double* nb = P.Yin + (size_t)(q >> 5) * NP * TILE + (q & 31);
-          const double xr = __ldg(nb + pr * TILE);
-          const double xi = diag ? 0.0 : __ldg(nb + pim * TILE);
+          const double* nb = P.Yin + (size_t)(q >> 5) * NP * TILE;
+          const double xr = __ldg(nb + at(pr, q & 31));
+          const double xi = diag ? 0.0 : __ldg(nb + at(pim, q & 31));
           ar += cb * xr - ca * xi;
           ai += cb * xi + ca * xr;
         }
@@ -162,8 +176,8 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
         const int m = mj * P.kp1 + kk;
         const int p = s_plus[m * TILE + lane];
         if (!diag && p >= 0) {  // - 1j * sig[p][i,j]
-          const double* nb = P.Yin + (size_t)(p >> 5) * NP * TILE + (p & 31);
-          const double xr = __ldg(nb + pr * TILE), xi = __ldg(nb + pim * TILE);
+          const double* nb = P.Yin + (size_t)(p >> 5) * NP * TILE;
+          const double xr = __ldg(nb + at(pr, p & 31)), xi = __ldg(nb + at(pim, p & 31));
           ar += xi;
           ai -= xr;
         }
@@ -171,9 +185,9 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
         if (q >= 0) {  // + n (b - 1j a) sig[q][i,j]
           const double n = (double)s_nv[m * TILE + lane];
           const double cb = n * P.b[kk], ca = n * P.a[kk];
-          const double* nb = P.Yin + (size_t)(q >> 5) * NP * TILE + (q & 31);
-          const double xr = __ldg(nb + pr * TILE);
-          const double xi = diag ? 0.0 : __ldg(nb + pim * TILE);
+          const double* nb = P.Yin + (size_t)(q >> 5) * NP * TILE;
+          const double xr = __ldg(nb + at(pr, q & 31));
+          const double xi = diag ? 0.0 : __ldg(nb + at(pim, q & 31));
           ar += cb * xr + ca * xi;
           ai += cb * xi - ca * xr;
         }
@@ -196,24 +210,24 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
       yr = sr + P.coef * ar;
       yi = si + P.coef * ai;
     } else if (STAGE == 2 || STAGE == 3) {
-      const double gr = P.sig[obase + pr * TILE];
-      const double gi = diag ? 0.0 : P.sig[obase + pim * TILE];
+      const double gr = P.sig[tbase + at(pr, lane)];
+      const double gi = diag ? 0.0 : P.sig[tbase + at(pim, lane)];
       yr = gr + P.coef * ar;
       yi = gi + P.coef * ai;
     } else {
-      const double gr = P.sig[obase + pr * TILE];
-      const double gi = diag ? 0.0 : P.sig[obase + pim * TILE];
-      const double y2r = P.Y2[obase + pr * TILE], y3r = P.Y3[obase + pr * TILE];
-      const double y2i = diag ? 0.0 : P.Y2[obase + pim * TILE];
-      const double y3i = diag ? 0.0 : P.Y3[obase + pim * TILE];
+      const double gr = P.sig[tbase + at(pr, lane)];
+      const double gi = diag ? 0.0 : P.sig[tbase + at(pim, lane)];
+      const double y2r = P.Y2[tbase + at(pr, lane)], y3r = P.Y3[tbase + at(pr, lane)];
+      const double y2i = diag ? 0.0 : P.Y2[tbase + at(pim, lane)];
+      const double y3i = diag ? 0.0 : P.Y3[tbase + at(pim, lane)];
       const double w = P.dt / 6.0, third = 1.0 / 3.0;
       yr = gr + ((y2r - gr) + 2.0 * (y3r - gr) + (sr - gr)) * third + w * ar;
       yi = gi + ((y2i - gi) + 2.0 * (y3i - gi) + (si - gi)) * third + w * ai;
       const double a2 = yr * yr + yi * yi;
       maxa2 = fmax(maxa2, a2);
     }
-    P.Yout[obase + pr * TILE] = yr;
-    if (!diag) P.Yout[obase + pim * TILE] = yi;
+    P.Yout[tbase + at(pr, lane)] = yr;
+    if (!diag) P.Yout[tbase + at(pim, lane)] = yi;
   }
 
   if (STAGE == 4) {
@@ -259,10 +273,9 @@ __global__ void k_pack(const KParams P, const double* __restrict__ ref, const in
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)P.n_tiles * TILE * NP;
   if (idx >= total) return;
-  const int lane = idx & 31;
-  const int64_t rest = idx >> 5;
-  const int p = rest % NP;
-  const int64_t tile = rest / NP;
+  const int64_t tile = idx / (NP * TILE);
+  int p, lane;
+  slot_info<D, HERM>((int)(idx % (NP * TILE)), p, lane);
   const int64_t r = tile * TILE + lane;
   double v = 0.0;
   if (r < P.n_tot) {
@@ -286,14 +299,16 @@ __global__ void k_unpack(const KParams P, const double* __restrict__ src, const 
   const int e = idx % (D * D);
   const int i = e / D, j = e % D;
   const int64_t k = dev2ref[r];
-  const int64_t s0 = (r >> 5) * Lay<D, HERM>::NP * TILE + (r & 31);
-  auto s = [&](int64_t off) -> double {  // float state when HB_PREC_SINGLE
-    return P.single ? (double)reinterpret_cast<const float*>(src)[s0 + off] : src[s0 + off];
+  const int64_t s0 = (r >> 5) * Lay<D, HERM>::NP * TILE;
+  const int ln = (int)(r & 31);
+  auto s = [&](int plane) -> double {  // float state when HB_PREC_SINGLE
+    const int64_t o = s0 + plane_off(HERM, D, plane, ln);
+    return P.single ? (double)reinterpret_cast<const float*>(src)[o] : src[o];
   };
   double re, im;
   if (HERM) {
     if (i == j) {
-      re = s(i * TILE);
+      re = s(i);
       im = 0.0;
     } else {
       const int a = i < j ? i : j, b = i < j ? j : i;
@@ -301,13 +316,13 @@ __global__ void k_unpack(const KParams P, const double* __restrict__ src, const 
       for (int rr = 0; rr < a; ++rr) ee += D - 1 - rr;
       ee += b - a - 1;
       const int pr = D + 2 * (ee - D);
-      re = s(pr * TILE);
-      im = s((pr + 1) * TILE);
+      re = s(pr);
+      im = s(pr + 1);
       if (i > j) im = -im;
     }
   } else {
-    re = s((2 * e) * TILE);
-    im = s((2 * e + 1) * TILE);
+    re = s(2 * e);
+    im = s(2 * e + 1);
   }
   ref[(k * D * D + e) * 2] = re;
   ref[(k * D * D + e) * 2 + 1] = im;
