@@ -295,18 +295,50 @@ def propagate(system: ExcitonSystem, bath: BathParams, rates: MarkovRates,
 
 def auto_truncate(system: ExcitonSystem, bath: BathParams, rates: MarkovRates,
                   config: PropagationConfig, initial_site: int = 1, tol_ps: float = 0.02,
-                  start_n: int = 2, n_cap: int = 20) -> tuple:
-    """Raise n_max until consecutive trapping times agree within tol_ps."""
+                  start_n: int = 2, n_cap: int = 20, speculate: bool = True) -> tuple:
+    """Raise n_max until consecutive trapping times agree within tol_ps
+    (heom.py:422-446; same return value, same ConvergenceFailure message).
+
+    With ``speculate`` the run of tier n + 2 starts on the GPU while tiers n and
+    n + 1 are compared (each run is its own handle and stream; small hierarchies
+    leave most SMs idle, so the two overlap).  The result is the same as the
+    serial search: the speculative run is only used when the search reaches it,
+    and an error it raised surfaces only then.  A speculative run still in
+    flight when the search stops is waited for (a device run is not cancelled).
+    """
     if tol_ps <= 0:
         raise ValueError("tolerance must be > 0")
     n = 0 if bath.lam_cm1 == 0 else max(0, start_n)
-    prev = propagate(system, bath, rates, replace(config, n_max=n), initial_site)
-    prev_t = trapping_time(prev)
-    while n < n_cap:
-        cur = propagate(system, bath, rates, replace(config, n_max=n + 1), initial_site)
-        cur_t = trapping_time(cur)
-        if abs(cur_t - prev_t) <= tol_ps:
-            return n, prev
-        n += 1
-        prev, prev_t = cur, cur_t
+
+    def run(k):
+        return propagate(system, bath, rates, replace(config, n_max=k), initial_site)
+
+    if not speculate:
+        prev = run(n)
+        prev_t = trapping_time(prev)
+        while n < n_cap:
+            cur = run(n + 1)
+            cur_t = trapping_time(cur)
+            if abs(cur_t - prev_t) <= tol_ps:
+                return n, prev
+            n += 1
+            prev, prev_t = cur, cur_t
+        raise ConvergenceFailure(f"trapping time not converged to {tol_ps} ps by n_max = {n_cap}")
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=2) as pool:
+        fut = {n: pool.submit(run, n)}
+        if n < n_cap:
+            fut[n + 1] = pool.submit(run, n + 1)
+        prev = fut.pop(n).result()
+        prev_t = trapping_time(prev)
+        while n < n_cap:
+            if n + 2 <= n_cap and n + 2 not in fut:
+                fut[n + 2] = pool.submit(run, n + 2)  # speculative
+            cur = fut.pop(n + 1).result()
+            cur_t = trapping_time(cur)
+            if abs(cur_t - prev_t) <= tol_ps:
+                return n, prev
+            n += 1
+            prev, prev_t = cur, cur_t
     raise ConvergenceFailure(f"trapping time not converged to {tol_ps} ps by n_max = {n_cap}")

@@ -284,12 +284,89 @@ def single_precision():
     (OUT / "traj_single.json").write_text(json.dumps(meta, indent=1))
 
 
+def auto_truncate_cases():
+    """heom.auto_truncate (heom.py:422-446) on the reference's own cases
+    (test_heom.py:299-324): the returned tier, its trajectory and the trapping
+    times of every tier the search visited."""
+    fmo = xf.build_fmo_system()
+    rates = xf.MarkovRates.from_inverse_ps(2.5, 250.0)
+    arrays, meta = {}, {"source": "excitonflow.heom.auto_truncate (heom.py:422-446), "
+                                  "cases of test_heom.py:299-324"}
+    import warnings
+    cases = {
+        "pairwise": (xf.BathParams.from_timescale(5.0, 166.0, 300.0),
+                     dict(dt_fs=10.0, n_max=0, residual=1e-5, hard_cap_fs=500000.0, record_stride=5),
+                     dict(start_n=1, tol_ps=0.5)),
+        "zero_coupling": (xf.BathParams.from_timescale(0.0, 166.0, 300.0),
+                          dict(dt_fs=5.0, n_max=0, t_end_fs=20000.0, residual=None, record_stride=10),
+                          dict()),
+        "fmo35_tol": (xf.BathParams.from_timescale(35.0, 166.0, 300.0),
+                      dict(dt_fs=10.0, n_max=0, residual=1e-5, hard_cap_fs=500000.0, record_stride=5),
+                      dict(start_n=1, tol_ps=0.2)),
+    }
+    for name, (bath, ckw, akw) in cases.items():
+        cfg = xf.PropagationConfig(**ckw)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            n, traj = xf.auto_truncate(fmo, bath, rates, cfg, 1, **akw)
+            visited = {}
+            lo = 0 if bath.lam_cm1 == 0 else akw.get("start_n", 2)
+            for k in range(lo, n + 2):
+                visited[str(k)] = float(xf.trapping_time(
+                    xf.propagate(fmo, bath, rates, xf.PropagationConfig(**{**ckw, "n_max": k}), 1)))
+        _traj_arrays(f"at_{name}", traj, arrays, meta)
+        meta[f"at_{name}"].update(n=int(n), trapping_times=visited, config=ckw, kwargs=akw,
+                                  bath=[bath.lam_cm1, 1.0 / bath.gamma_fs1, bath.temperature_k])
+    try:  # the cap failure message (test_heom.py:319-324)
+        xf.auto_truncate(fmo, xf.BathParams.from_timescale(35.0, 166.0, 300.0), rates,
+                         xf.PropagationConfig(dt_fs=5.0, n_max=0, t_end_fs=500.0, residual=None),
+                         1, tol_ps=1e-12, start_n=0, n_cap=2)
+    except xf.ConvergenceFailure as exc:
+        meta["cap_failure_message"] = str(exc)
+    np.savez_compressed(OUT / "auto_truncate.npz", **arrays)
+    (OUT / "auto_truncate.json").write_text(json.dumps(meta, indent=1))
+
+
+def cli_artifacts():
+    """The `excitonflow propagate` CSV (cli.py:287-293, 396-415) for two runs, and
+    the emitted config header (cli.py:210-219) of a few configurations."""
+    from dataclasses import replace as dc_replace
+    from excitonflow import cli
+    out = {"source": "excitonflow.cli.main propagate / cli.emit_config (cli.py:210-219, 396-415)",
+           "runs": {}, "headers": {}}
+    runs = {"n2_t200": ["propagate", "--n-max", "2", "--t-end-fs", "200", "--residual", "none"],
+            "site6_lam55": ["propagate", "--n-max", "3", "--t-end-fs", "100", "--residual", "none",
+                            "--site", "6", "--lambda-cm1", "55", "--record-stride", "4"]}
+    for name, argv in runs.items():
+        path = Path("/tmp") / f"golden_cli_{name}.csv"
+        assert cli.main(argv + ["--out", str(path)]) == 0
+        out["runs"][name] = {"argv": argv, "csv": path.read_text()}
+    base = cli.RunConfig()
+    cfgs = {"default": base,
+            "auto": dc_replace(base, n_max=None, t_end_fs=1000.0, residual=None, workers=4),
+            "sweep": dc_replace(base, lambdas=(10.0, 35.5), sites=(1, 6), n_max_list=(2, 4),
+                                add_reorg_to_diagonal=True, precision="single")}
+    for name, c in cfgs.items():
+        out["headers"][name] = {"fields": {k: (list(v) if isinstance(v, tuple) else v)
+                                           for k, v in c.__dict__.items()},
+                                "lines": cli.emit_config(c)}
+    (OUT / "cli_artifacts.json").write_text(json.dumps(out, indent=1))
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--cli", action="store_true", help="only the CLI artifact fixtures")
+    ap.add_argument("--auto-truncate", action="store_true", help="only the auto_truncate cases")
     ap.add_argument("--single", action="store_true", help="only the precision='single' runs")
     ap.add_argument("--long", action="store_true", help="only the N_max=6 eta run")
     ap.add_argument("--dense", action="store_true", help="only the dense heom_rhs fixtures")
     args = ap.parse_args()
+    if args.cli:
+        cli_artifacts()
+        return
+    if args.auto_truncate:
+        auto_truncate_cases()
+        return
     if args.single:
         single_precision()
         return
@@ -304,6 +381,8 @@ def main():
     dense_cases()
     trajectories(long=False)
     single_precision()
+    auto_truncate_cases()
+    cli_artifacts()
 
 
 if __name__ == "__main__":

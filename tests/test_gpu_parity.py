@@ -367,3 +367,38 @@ def test_other_shapes_match_oracle(n, K, n_max, ground):
     assert np.array_equal(traj.times_fs, ref["times_fs"])
     assert np.max(np.abs(traj.populations - ref["populations"])) < 1e-10
     assert np.max(np.abs(traj.matrices - ref["matrices"])) < 1e-10
+
+
+def test_nccl_shard_path_world_one_is_bit_exact():
+    """The NCCL sharded path (hb_nccl_init, hb_shard_steps: launch groups, second
+    stream, guard all-reduce) at world size 1 -- the only size one GPU can run --
+    equals the unsharded run bit for bit; multi-GPU halos are covered by the
+    in-process shards above and the gloo protocol test (tests/test_shard_host.py)."""
+    import socket
+    import torch.distributed as dist
+    from paper_1012_4382_b200.shard import NcclShardedRun
+    ops = BlockOperands(FMO, BATH300, RATES, 1)
+    rho0 = np.zeros((7, 7), complex)
+    rho0[0, 0] = 1.0
+    with DeviceRun(ops, 4, 1.0, t_end_fs=60.0, layout="hermitian") as ref:
+        ref.set_rho0(rho0, [0.0, 0.0])
+        assert ref.run() == N.HB_OK
+        _, pops_ref, _ = ref.records()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        sr = NcclShardedRun(ops, 4, 1.0, 60.0, 0, 1, 0, dist, record_stride=1)
+        try:
+            sr.set_rho0(rho0, [0.0, 0.0])
+            assert sr.run(chunk=25) == 1
+            _, pops, _ = sr.run_.records()
+            assert sr.describe()["halo_ados_max"] == 0
+            assert sr.launch_count() > 0
+        finally:
+            sr.close()
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(pops, pops_ref)
