@@ -10,12 +10,15 @@ reference relies on numba's nogil for the same, cli.py:279-284).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 LIB_NAME = "libheomb200.so"
-LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+#: HEOM_B200_LIB selects another build of the same library (the test-suite's
+#: bounds-checked libheomb200_checked.so); default: the in-tree release build
+LIB_PATH = Path(os.environ.get("HEOM_B200_LIB") or Path(__file__).resolve().parent / LIB_NAME)
 
 HB_OK, HB_ERR_ARG, HB_ERR_CUDA, HB_DIVERGED, HB_HARDCAP, HB_ERR_RANGE = 0, 1, 2, 3, 4, 5
 HB_STOP_NONE, HB_STOP_T_END, HB_STOP_RESIDUAL = 0, 1, 2

@@ -180,6 +180,7 @@ static int rhs_impl(double* out, const double* sig, int64_t n_tot, int d, const 
   p.modes = modes;
   p.n_tot = (int)n_tot;
   p.n_tiles = gt.n_tiles;
+  p.n_tiles_total = gt.n_tiles;
   p.hermitian = 0;
   p.n_planes = 2 * d * d;
   for (int i = 0; i < d; ++i) {

@@ -26,6 +26,7 @@ __global__ void k_halo_pack(const T* __restrict__ buf, int n, const int32_t* __r
   const int e = (int)(idx / nc), q = (int)(idx % nc);
   const int t = pos[e];
   const int p = planes[site[e] * nc + q];
+  HB_CHECK(t >= 0 && p >= 0 && p < n_planes);
   out[idx] = buf[(size_t)(t >> 5) * n_planes * TILE + herm_off(d, p, t & 31)];
 }
 
@@ -38,6 +39,7 @@ __global__ void k_halo_unpack(T* __restrict__ buf, int n, const int32_t* __restr
   const int e = (int)(idx / nc), q = (int)(idx % nc);
   const int t = pos[e];
   const int p = planes[site[e] * nc + q];
+  HB_CHECK(t >= 0 && p >= 0 && p < n_planes);
   buf[(size_t)(t >> 5) * n_planes * TILE + herm_off(d, p, t & 31)] = in[idx];
 }
 

@@ -4,6 +4,16 @@
 #include <cuda_runtime.h>
 #include "heom_b200.h"
 
+// HB_CHECKED (build target libheomb200_checked.so, tests only): device-side
+// bounds checks on every gathered position, tile index and halo slot -- the
+// substitute for compute-sanitizer, which is closed on the GPU pool.
+#ifdef HB_CHECKED
+#include <cassert>
+#define HB_CHECK(cond) assert(cond)
+#else
+#define HB_CHECK(cond) ((void)0)
+#endif
+
 namespace hb {
 
 constexpr int TILE = 32;          // ADOs per tile (AoSoA inner extent = one warp)

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(32, CAP ? 12 : 1) k_mm4(const KParams P) {
   if (ctl->status != ST_RUNNING) return;
   const int lane = threadIdx.x;
   const int tile = P.tile_list ? P.tile_list[blockIdx.x] : P.tile_begin + blockIdx.x;
+  HB_CHECK(tile >= 0 && tile < P.n_tiles_total);
   const size_t tb = (size_t)tile * TB;  // element offset of the tile
   const T c = (T)(STAGE == 4 ? P.dt / 6.0 : P.coef);
   const bool top = tile >= P.top_tile;

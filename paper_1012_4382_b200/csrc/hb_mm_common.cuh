@@ -271,7 +271,10 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c, b
     return r;
   };
   // link target t (position): its tile base and its lane
-  auto tbase = [&](int t) -> const T* { return yin + (size_t)(t >> 5) * TB; };
+  auto tbase = [&](int t) -> const T* {
+    HB_CHECK(t < 0 || t < P.n_tiles_total * TILE);
+    return yin + (size_t)(t >> 5) * TB;
+  };
   if (no_up) {
 #pragma unroll
     for (int s0 = 0; s0 < D; s0 += GROUP) {

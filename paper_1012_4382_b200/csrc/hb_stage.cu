@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
   }
   const int tile = P.tile_begin + blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  HB_CHECK(tile < P.n_tiles_total);
   const int M = P.modes;
   int32_t* s_plus = reinterpret_cast<int32_t*>(smem_raw);
   int32_t* s_minus = s_plus + M * TILE;
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
       for (int kk = 0; kk < P.kp1; ++kk) {
         const int m = mi * P.kp1 + kk;
         const int p = s_plus[m * TILE + lane];
+        HB_CHECK(p < P.n_tiles_total * TILE);
         if (!diag && p >= 0) {  // + 1j * sig[p][i,j]
           const double* nb = P.Yin + (size_t)(p >> 5) * NP * TILE;
           const double xr = __ldg(nb + at(pr, p & 31)), xi = __ldg(nb + at(pim, p & 31));
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
           ai += xr;
         }
         const int q = s_minus[m * TILE + lane];
+        HB_CHECK(q < P.n_tiles_total * TILE);
         if (q >= 0) {  // + n (b + 1j a) sig[q][i,j]
           const double n = (double)s_nv[m * TILE + lane];
           const double cb = n * P.b[kk], ca = n * P.a[kk];
