@@ -1,5 +1,4 @@
-for f in 0 100000; do
-  HB_FOLD_EXP=$f python tools/small_probe.py 0 3000 | sed "s/^/[fold<=$f] /"
-  HB_FOLD_EXP=$f python tools/small_probe.py 1 2000 | sed "s/^/[fold<=$f] /"
-  HB_FOLD_EXP=$f HB_SWEEP_NMAX=8 timeout 120 python tools/kernel_sweep.py 200 | sed "s/^/[fold<=$f] /" | cut -c1-150
+for r in 1 2; do
+  timeout 120 python tools/kernel_sweep.py 200 | sed "s/^/[base] /" | cut -c1-170
+  HB_ORDER_EXP=1 timeout 120 python tools/kernel_sweep.py 200 | sed "s/^/[A,top,t7] /" | cut -c1-170
 done
