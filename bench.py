@@ -72,11 +72,19 @@ def dist_env():
     return world, rank, local
 
 
-def init_dist(world, local, backend):
-    if world <= 1:
-        return None
+def init_dist(world, local, backend, single=False):
+    """torch.distributed for N > 1 (torchrun's env); with `single`, a one-rank
+    group (the sharded code path at world size 1)."""
     import torch
     import torch.distributed as dist
+    if world <= 1:
+        if not single:
+            return None
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+        return dist
     if backend == "nccl":
         torch.cuda.set_device(local)
     dist.init_process_group(backend=backend)
@@ -388,7 +396,8 @@ def sweep_sample(xf, device, rank, world, n_points):
 def run_b200(args):
     world, rank, local = dist_env()
     import torch
-    dist = init_dist(world, local, "nccl" if torch.cuda.is_available() else "gloo")
+    dist = init_dist(world, local, "nccl" if torch.cuda.is_available() else "gloo",
+                     single=args.force_shard)
     device = local
     torch.cuda.set_device(device)
     xf, system, bath, rates = workload()
@@ -399,7 +408,7 @@ def run_b200(args):
     peak = peaks.get("hbm_gbs", 6650.0)
 
     shard = None
-    if world > 1 and not args.replicas:
+    if (world > 1 and not args.replicas) or args.force_shard:
         try:
             shard = run_sharded(args, dist, world, rank, local, xf, ops)
         except Exception as exc:  # report it, keep the replica number
@@ -430,6 +439,15 @@ def run_b200(args):
     except Exception as exc:
         single = {"error": str(exc)}
 
+    # device time of 1000 resident steps (same length as the longer e2e run: the
+    # clock settles lower over a longer run than over the K timed steps)
+    run_l = DeviceRun(ops, N_MAX, DT, t_end_fs=1e15, record_stride=10 ** 12, device=device)
+    rho0_l = np.zeros((D, D), complex)
+    rho0_l[0, 0] = 1.0
+    run_l.set_rho0(rho0_l, [0.0, 0.0])
+    run_l.time_steps(max(3, args.warmup))
+    ms_1000 = run_l.time_steps(1000) / 1000
+    run_l.close()
     e2e = {}
     for steps in (50, 1000):
         wall, (bi, bo) = e2e_measure(xf, system, bath, rates, device, steps, dist, local)
@@ -506,6 +524,8 @@ def run_b200(args):
                     "api": "paper_1012_4382_b200.propagate (t_end run, a record every step)",
                     "steps_1000": {"value": e2e[1000]["value"],
                                    "frac_of_value": e2e[1000]["value"] / (value_1 * world),
+                                   "device_ms_per_step_1000": ms_1000,
+                                   "frac_of_device_1000": e2e[1000]["value"] / (N_ADO / (ms_1000 / 1e3) * world),
                                    "h2d_bytes_per_step": e2e[1000]["h2d_bytes_per_step"],
                                    "d2h_bytes_per_step": e2e[1000]["d2h_bytes_per_step"]}},
             "gpu_launches": int(launches),
@@ -515,7 +535,7 @@ def run_b200(args):
             "clocks": clk,
             "cpu_baseline": cpu,
         }
-        if world > 1:
+        if world > 1 or args.force_shard:
             line["replicas"] = {"value": value_1 * world, "ms_per_step": ms_step, "scaling": "weak"}
             if shard is not None and "value" in shard:
                 line.update(value=shard["value"], ms_per_step=shard["ms_per_step"],
@@ -578,6 +598,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas only (no sharded run)")
+    ap.add_argument("--force-shard", action="store_true",
+                    help="run the sharded path even at one rank (tests the NCCL code path)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-reference", action="store_true",
                     help="skip the numba reference inside the cpu_baseline")

@@ -67,6 +67,7 @@ struct hb_handle {
   int own_tiles = 0;          // tiles [0, own_tiles) are computed here; the rest is halo
   int32_t* groups = nullptr;  // device tile lists of the four launch groups
   int group_off[5] = {0, 0, 0, 0, 0};
+  int group_first[4] = {-1, -1, -1, -1};  // first tile of a contiguous group, else -1
   void* nccl_comm = nullptr;
   cudaStream_t comm = nullptr;  // halo exchange + guard all-reduce stream
   // events: ev_send[s-1] stage s's send tiles done (compute); ev_halo[b] halo of

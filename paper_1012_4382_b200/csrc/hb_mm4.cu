@@ -178,7 +178,8 @@ static cudaError_t mm4_kp1(int stage, const KParams& p, cudaStream_t s) {
 }
 
 // the stage kernel alone (sharded runs launch a stage as several tile groups and
-// the step bookkeeping once after the last)
+// the step bookkeeping once after the last); a group that is one contiguous
+// ascending run of tiles is launched as a range (no per-CTA tile-list load)
 template <int D, int KP1>
 static cudaError_t mm4_only_t(int stage, const KParams& p, cudaStream_t s) {
   return p.single ? mm4_stage<float, D, KP1>(stage, p, s) : mm4_stage<double, D, KP1>(stage, p, s);

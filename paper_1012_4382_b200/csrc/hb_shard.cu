@@ -107,7 +107,11 @@ cudaError_t launch_group(hb_handle* h, int stage, int g, cudaStream_t s, int* n_
   const int n = h->group_off[g + 1] - h->group_off[g];
   if (n == 0) return cudaSuccess;
   KParams p = stage_params(h, stage);
-  p.tile_list = h->groups + h->group_off[g];
+  if (h->group_first[g] >= 0) {  // a contiguous run of tiles: a plain range launch
+    p.tile_begin = h->group_first[g];
+  } else {
+    p.tile_list = h->groups + h->group_off[g];
+  }
   p.n_tiles = n;
   ++*n_launched;
   return launch_mm4_only(stage, p, s);
@@ -169,6 +173,12 @@ int init_shard(hb_handle* h, const hb_shard_tables* T) {
     total += T->group_count[g];
   }
   h->group_off[4] = total;
+  for (int g = 0; g < 4; ++g) {  // contiguous ascending groups launch as ranges
+    const int32_t* t = T->groups + h->group_off[g];
+    bool run = T->group_count[g] > 0;
+    for (int i = 1; i < T->group_count[g] && run; ++i) run = t[i] == t[0] + i;
+    h->group_first[g] = run ? t[0] : -1;
+  }
   CK(cudaMalloc(&h->groups, (size_t)(total > 0 ? total : 1) * sizeof(int32_t)));
   CK(hb_memcpy(h->groups, T->groups, (size_t)total * sizeof(int32_t), cudaMemcpyHostToDevice,
                h->stream));
@@ -331,10 +341,18 @@ int hb_shard_steps(hb_handle* h, int64_t n_steps, double* ms) {
     if (rc) return rc;
     h->halo_primed = true;
   }
+  // a shard without a halo plan (one rank) runs its stages back to back, keeping
+  // the programmatic-launch overlap between them
+  bool has_halo = false;
+  for (size_t i = 0; i < h->halo.count.size(); ++i) has_halo = has_halo || h->halo.count[i] > 0;
   for (int64_t it = 0; it < n_steps; ++it) {
     int n_launched = 0;
     for (int s = 1; s <= 4; ++s) {
       const int b_in = s - 1, b_out = s % 4;
+      if (!has_halo) {
+        for (int g = 0; g < 4; ++g) CK(launch_group(h, s, g, h->stream, &n_launched));
+        continue;
+      }
       // the previous pack of b_out must have read it before this stage rewrites it
       if (h->packed_once[b_out]) CK(cudaStreamWaitEvent(h->stream, h->ev_packed[b_out], 0));
       CK(launch_group(h, s, 0, h->stream, &n_launched));

@@ -5,10 +5,10 @@ Partition.  The ADOs are split into contiguous ranges of the pure
 lexicographic order (n -> n + e_m preserves it, so a range keeps most of its
 neighbours: at N_max = 8, K = 1, P = 8 a shard needs 8.6 MB of crosses per stage
 against 59 MB for ranges of the reference's tier-major order).  Inside a shard
-the owned ADOs are renumbered: those below the top tier first, then the top-tier
-ones in whole tiles -- tiles with no raise links, which the production kernel
-gathers in paired-site rounds (csrc/hb_mm4.cu) -- then halo slots for the
-neighbours owned elsewhere.  A shard's buffers hold only its owned and halo
+the owned ADOs are renumbered: those below the top tier first, tier-major like
+the reference order, then the top-tier ones in whole tiles -- tiles with no
+raise links, which the production kernel gathers in paired-site rounds
+(csrc/hb_mm4.cu) -- then halo slots for the neighbours owned elsewhere.  A shard's buffers hold only its owned and halo
 slots (``ShardLayout``).
 
 Halo.  A kernel reads, from a neighbour reached through mode m, only the cross
@@ -109,7 +109,13 @@ def build_shards(indices, tiers, plus, minus, n_shards: int, kp1: int, n_max: in
     for q in range(n_shards):
         own = order[bounds[q]:bounds[q + 1]]
         top = tiers[own] == n_max
-        low_part, top_part = own[~top], own[top]
+        # below the top tier: tier-major, lexicographic inside a tier (the
+        # reference's own order restricted to the shard: the L2 window over these
+        # tiles then holds the gather targets of the top tier); the top tier in
+        # whole tiles after them
+        low_part = own[~top]
+        low_part = low_part[np.argsort(tiers[low_part], kind="stable")]
+        top_part = own[top]
         a_tiles = -(-len(low_part) // TILE)
         own_tiles = a_tiles + -(-len(top_part) // TILE)
         # neighbours owned elsewhere, with the site they are reached through
@@ -341,6 +347,7 @@ class NcclShardedRun(_ShardBase):
         return self.sync()[0]
 
     def launch_count(self) -> int:
+        self.sync()  # the device-counted step kernels are read at a synchronisation
         return self.run_.launch_count()
 
     def describe(self) -> dict:
