@@ -393,8 +393,25 @@ def sweep_sample(xf, device, rank, world, n_points):
                     "residual 1e-5, dt 1.25 fs"}
 
 
+def nccl_log_lines(limit=12):
+    """The NCCL INIT log of this process (NCCL_DEBUG=INFO written to a file, so
+    stdout keeps one JSON line): version, transports, communicator init."""
+    path = Path(tempfile.gettempdir()) / f"hb_nccl_{os.getpid()}.log"
+    if not path.exists():
+        return None
+    keep = [l.strip() for l in path.read_text(errors="replace").splitlines()
+            if "NCCL INFO" in l and any(k in l for k in ("version", "Init", "NVLS", "P2P", "nranks",
+                                                         "Channel 00", "NVLink", "Connected"))]
+    maps = [l.split()[-1] for l in open("/proc/self/maps") if "libnccl" in l]
+    return {"library": sorted(set(maps)), "lines": keep[:limit]}
+
+
 def run_b200(args):
     world, rank, local = dist_env()
+    if world > 1 or args.force_shard:  # NCCL communicator init visible, off stdout
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT,P2P,NVLS"
+        os.environ["NCCL_DEBUG_FILE"] = str(Path(tempfile.gettempdir()) / f"hb_nccl_{os.getpid()}.log")
     import torch
     dist = init_dist(world, local, "nccl" if torch.cuda.is_available() else "gloo",
                      single=args.force_shard)
@@ -537,6 +554,7 @@ def run_b200(args):
         }
         if world > 1 or args.force_shard:
             line["replicas"] = {"value": value_1 * world, "ms_per_step": ms_step, "scaling": "weak"}
+            line["nccl_init_log_rank0"] = nccl_log_lines()
             if shard is not None and "value" in shard:
                 line.update(value=shard["value"], ms_per_step=shard["ms_per_step"],
                             scaling="strong", config=config_dict(world, sharded=True),
