@@ -486,7 +486,7 @@ constexpr size_t kGraphCacheCap = 8;
 constexpr int kGraphsPerSync = 2;
 // RK4 steps per WHILE-body (PDL-chained inside a body; a run stops within the
 // body of its stop step)
-constexpr int kDefaultBodySteps = 4;
+constexpr int kDefaultBodySteps = 16;
 
 
 static void graph_cache_put(hb_handle* h) {
