@@ -1,0 +1,9 @@
+set -x
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f_smoke.log 2>&1; echo smoke=$?
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/f_tests.log 2>&1; echo tests=$?
+tail -3 gpurun_out/f_tests.log
+python bench.py > gpurun_out/f_bench.json 2> gpurun_out/f_bench.err; echo bench=$?
+python bench.py --impl reference > gpurun_out/f_bench_ref.json 2> gpurun_out/f_bench_ref.err; echo ref=$?
+tail -c 600 gpurun_out/f_bench.json
