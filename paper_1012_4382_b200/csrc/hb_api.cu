@@ -711,6 +711,15 @@ static int create_impl(const hb_params* P, const hb_shard_tables* T, hb_handle**
     const int64_t first_top = n_tot - top_count;
     p.top_tile = (int)((first_top + TILE - 1) / TILE);
   }
+  // small hierarchies: k_mm4ab (phase A and phase B of a tile on separate warps,
+  // hb_mm4.cu) while the tiles fill at most ~4 per SM; decided on the whole
+  // hierarchy's size, so every shard of a run makes the same choice
+  {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    const int64_t all_tiles = (hierarchy_size(modes, q.n_max) + TILE - 1) / TILE;
+    p.split = d > 7 || sms <= 0 ? 0 : all_tiles <= sms ? 2 : all_tiles <= 4 * sms ? 1 : 0;
+  }
   // L2 persisting window over the stage input's tiers below N_max (tier-major
   // order: one contiguous prefix, 36 % of the ADOs at N_max = 8, K = 1): the
   // targets of the top tier's lower-link gathers stay in L2 while the state

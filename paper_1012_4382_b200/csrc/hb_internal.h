@@ -85,6 +85,9 @@ struct KParams {
   const uint8_t* nvec;
   const double* damp_plane;  // optional per-ADO damping (Level-2 shim), else null
   int fast;                  // production kernel k_mm4 (hb_mm4.cu), else the generic k_stage
+  int split;                 // small hierarchies (fast path, d <= 7): a tile's phase A and
+                             // phase B on separate warps, k_mm4ab: 1 = 1 + 1 warps,
+                             // 2 = 2 + 2 warps; 0 = k_mm4 (one warp per tile)
   int top_tile;              // first tile whose ADOs all sit on the top tier (no raise
                              // links; tier-major order), n_tiles_total if none
   const int32_t* tile_list;  // if set: block b computes tile tile_list[b] (sharded

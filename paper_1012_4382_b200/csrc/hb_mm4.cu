@@ -82,6 +82,134 @@ __global__ void __launch_bounds__(32, CAP ? 12 : 1) k_mm4(const KParams P) {
   }
 }
 
+
+// k_mm4ab: the stage kernel for small hierarchies (KParams::split; at most a
+// few tiles per SM).  There one warp per tile leaves three of an SM's four
+// sub-partitions idle and the tile's chain is the stage time: phase A (the
+// commutator, ~850 instructions, FP64-issue bound in one warp) then phase B (the
+// link crosses, 4-7 dependent gather rounds).  Here NA warps run phase A on
+// disjoint row ranges of the ADO while NB warps run phase B on disjoint site
+// ranges, each from its own zeroed accumulator; the last warp adds the partial
+// sums from shared memory, (A + B_lo) + B_hi, and stores as k_mm4.  The same
+// phase functions as k_mm4 (hb_mm_common.cuh), so every element's RHS terms are
+// the reference's; only the grouping of the final sum differs from k_mm4 (equal
+// to the last bits).  The split is chosen from the size of the whole hierarchy,
+// so all shards of a run and the unsharded run use the same one.
+// Measured at the config-3 K = 0 twin (54 tiles): 19.7-20.6 vs 25.5-27.5 us per
+// step; K = 1, N_max = 4 (96 tiles): 26 vs 37; N_max = 5 (364 tiles, 1 + 1): 36
+// vs 43; above ~4 tiles per SM one warp per tile wins (N_max = 6: 58 vs 51).
+template <int D>
+__host__ __device__ constexpr int row_split() {  // balances ~3:1 off-diagonal : diagonal cost
+  int tot = 0;
+  for (int i = 0; i < D; ++i) tot += 3 * (D - 1 - i) + 1;
+  int acc = 0;
+  for (int r = 0; r < D; ++r) {
+    acc += 3 * (D - 1 - r) + 1;
+    if (2 * acc >= tot) return r + 1;
+  }
+  return D;
+}
+template <int D>
+__host__ __device__ constexpr int site_split() { return ((D + 1) / 2 + 1) / 2 * 2 < D ? ((D + 1) / 2 + 1) / 2 * 2 : D; }
+
+template <class T, int D, int KP1, int STAGE, int NA, int NB>
+__global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
+  constexpr int NP = D * D;
+  constexpr int M = D * KP1;
+  constexpr int TB = NP * TILE;
+  constexpr bool kInc = kIncScheme<T>;
+  constexpr int RS = NA == 2 ? row_split<D>() : D;
+  constexpr int SS = NB == 2 ? site_split<D>() : D;
+  __shared__ __align__(128) T sBase[(STAGE >= 2 || kInc ? NP : 1) * TILE];
+  __shared__ __align__(128) T sInc[(kInc && (STAGE == 2 || STAGE == 4) ? NP : 1) * TILE];
+  __shared__ __align__(128) T sXA[NP * TILE];
+  __shared__ __align__(128) T sXB[(NB == 2 ? NP : 1) * TILE];
+  __shared__ __align__(16) int32_t sUp[M][TILE];
+  __shared__ __align__(16) int32_t sDn[M][TILE];
+  __shared__ __align__(16) uint8_t sN[M][TILE];
+  __shared__ __align__(8) uint64_t bar;
+  volatile Ctl* ctl = P.ctl;
+  if (ctl->status != ST_RUNNING) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tile = P.tile_list ? P.tile_list[blockIdx.x] : P.tile_begin + blockIdx.x;
+  HB_CHECK(tile >= 0 && tile < P.n_tiles_total);
+  const size_t tb = (size_t)tile * TB;
+  const T c = (T)(STAGE == 4 ? P.dt / 6.0 : P.coef);
+  const bool top = tile >= P.top_tile;
+  if (warp == 0)
+    tile_prologue<T, D, KP1, STAGE>(P, tile, sBase, &sUp[0][0], &sDn[0][0], &sN[0][0], &bar, !top,
+                                    sInc, true);
+  __syncthreads();
+  pdl_wait();
+  if (warp == 0) tile_prologue_late<T, D, STAGE>(P, tile, sInc, &bar);
+  if (ctl->status != ST_RUNNING) {
+    mbar_wait(&bar, 0);
+    return;
+  }
+  pdl_release();
+  const long long step_next = ctl->step + 1;
+  T acc[NP];
+  auto put_rows = [&](auto r0, auto r1) {
+#pragma unroll
+    for (int i = decltype(r0)::value; i < decltype(r1)::value; ++i) {
+      sXA[i * TILE + lane] = acc[i];
+#pragma unroll
+      for (int j = i + 1; j < D; ++j) {
+        sXA[Pk<D>::re(i, j) * TILE + lane] = acc[Pk<D>::re(i, j)];
+        sXA[Pk<D>::im(i, j) * TILE + lane] = acc[Pk<D>::im(i, j)];
+      }
+    }
+  };
+  auto phase_b_part = [&](auto s0, auto s1) {
+    mbar_wait(&bar, 0);
+#pragma unroll
+    for (int e = 0; e < NP; ++e) acc[e] = 0;
+    bool no_up = top;
+    if (!top) {
+      bool up_any = false;
+#pragma unroll
+      for (int m = 0; m < M; ++m) up_any |= sUp[m][lane] >= 0;
+      no_up = !__any_sync(0xffffffffu, up_any);
+    }
+    phase_b_sites<T, D, KP1, 2, decltype(s0)::value, decltype(s1)::value>(P, lane, c, no_up, sUp,
+                                                                            sDn, sN, acc);
+  };
+  using Z = std::integral_constant<int, 0>;
+  using RSc = std::integral_constant<int, RS>;
+  using Dc = std::integral_constant<int, D>;
+  using SSc = std::integral_constant<int, SS>;
+  if (warp == 0) {
+    phase_a<T, D, KP1, STAGE, 0, RS>(P, tile, lane, c, sBase, sN, &bar, acc);
+    put_rows(Z(), RSc());
+  } else if (NA == 2 && warp == 1) {
+    phase_a<T, D, KP1, STAGE, RS, D>(P, tile, lane, c, sBase, sN, &bar, acc);
+    put_rows(RSc(), Dc());
+  } else if (NB == 2 && warp == NA) {
+    phase_b_part(Z(), SSc());
+#pragma unroll
+    for (int e = 0; e < NP; ++e) sXB[e * TILE + lane] = acc[e];
+  } else {
+    if constexpr (NB == 2) phase_b_part(SSc(), Dc());
+    else phase_b_part(Z(), Dc());
+  }
+  __syncthreads();
+  if (warp == NA + NB - 1) {
+#pragma unroll
+    for (int e = 0; e < NP; ++e)
+      acc[e] = NB == 2 ? (sXA[e * TILE + lane] + sXB[e * TILE + lane]) + acc[e]
+                       : sXA[e * TILE + lane] + acc[e];
+    double maxa2 = 0.0;
+    phase_c_store<T, D, STAGE>(P, lane, tb, sBase, acc, maxa2, sInc);
+    if (STAGE == 4 && step_next % 25 == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxa2 = fmax(maxa2, __shfl_xor_sync(0xffffffffu, maxa2, o));
+      if (lane == 0)
+        atomicMax(const_cast<unsigned long long*>(&ctl->maxabs2_bits),
+                  (unsigned long long)__double_as_longlong(maxa2));
+    }
+  }
+}
+
 // The per-step bookkeeping (sinks heom.py:382-383, guard heom.py:386-389,
 // records, stop policy heom.py:359-368) as its own one-warp kernel after stage
 // 4, chained by PDL: it waits for the stage-4 grid to complete and flush, so the
@@ -145,6 +273,16 @@ static cudaError_t mm4_go(const KParams& p, cudaStream_t s) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = n;
+  if constexpr (D <= 7) {  // (41.5 KB of static shared memory at d = 7, 2 + 2 warps)
+    if (p.split == 1) {
+      cfg.blockDim = dim3(64);
+      return cudaLaunchKernelEx(&cfg, k_mm4ab<T, D, KP1, STAGE, 1, 1>, p);
+    }
+    if (p.split == 2) {
+      cfg.blockDim = dim3(128);
+      return cudaLaunchKernelEx(&cfg, k_mm4ab<T, D, KP1, STAGE, 2, 2>, p);
+    }
+  }
   return cudaLaunchKernelEx(&cfg, k_mm4<T, D, KP1, STAGE, CAP>, p);
 }
 

@@ -132,7 +132,7 @@ __device__ __forceinline__ void pdl_release() {
 
 // phase A: acc = base + c (damping + commutator) with the ADO in registers.
 // sBase: the tile's base operand (flat, Hermitian tile layout).
-template <class T, int D, int KP1, int STAGE>
+template <class T, int D, int KP1, int STAGE, int R0 = 0, int R1 = D>
 __device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, T c, T* sBase,
                                         const uint8_t (*sN)[TILE], uint64_t* bar,
                                         T (&acc)[D * D]) {
@@ -148,7 +148,7 @@ __device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, T 
     s[D + 2 * e] = v.x;
     s[D + 2 * e + 1] = v.y;
   }
-  if (tile == 0 && lane == 0) {  // sink rates of this stage input (heom.py:282-283)
+  if (R0 == 0 && tile == 0 && lane == 0) {  // sink rates of this stage input (heom.py:282-283)
     int q = 0;
     for (int sk = 0; sk < P.n_sinks; ++sk) {
       double a = 0.0;
@@ -172,7 +172,7 @@ __device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, T 
   constexpr T third = (T)(1.0 / 3.0);
   constexpr bool kInc = kIncScheme<T>;
 #pragma unroll
-  for (int i = 0; i < D; ++i) {
+  for (int i = R0; i < R1; ++i) {
     // diagonal: Re(-i[H,s])_ii = 2 sum_{l != i} h_il Im s_il
     T cm = 0;
 #pragma unroll
@@ -245,7 +245,7 @@ __device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, T 
 // no_up (warp-uniform): no lane of the tile has a raise link (the top tier) --
 // the lower links of GROUP sites are gathered per round trip (the same loads as
 // one full site), halving the dependent rounds of the tile.
-template <class T, int D, int KP1, int GROUP = 2>
+template <class T, int D, int KP1, int GROUP = 2, int S0 = 0, int S1 = D>
 __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c, bool no_up,
                                               const int32_t (*sUp)[TILE],
                                               const int32_t (*sDn)[TILE],
@@ -277,9 +277,9 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c, b
   };
   if (no_up) {
 #pragma unroll
-    for (int s0 = 0; s0 < D; s0 += GROUP) {
+    for (int s0 = S0; s0 < S1; s0 += GROUP) {
 #pragma unroll
-      for (int st = s0; st < (s0 + GROUP < D ? s0 + GROUP : D); ++st) {
+      for (int st = s0; st < (s0 + GROUP < S1 ? s0 + GROUP : S1); ++st) {
 #pragma unroll
         for (int k = 0; k < KP1; ++k) {
           const int m = st * KP1 + k;
@@ -310,7 +310,7 @@ __device__ __forceinline__ void phase_b_sites(const KParams& P, int lane, T c, b
     return;
   }
 #pragma unroll
-  for (int st = 0; st < D; ++st) {
+  for (int st = S0; st < S1; ++st) {
 #pragma unroll
     for (int k = 0; k < KP1; ++k) {
       const int m = st * KP1 + k;

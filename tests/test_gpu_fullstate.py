@@ -78,9 +78,13 @@ def _case(K, n_max, steps):
     return _CACHE[key]
 
 
+# kernels by size (hb_api.cu KParams::split): N_max = 3, 4 -> k_mm4ab 2 + 2 warps;
+# K = 0, N_max = 8 (202 tiles) and K = 1, N_max = 5 (364 tiles) -> 1 + 1 warps;
+# K = 1, N_max = 8 -> k_mm4 (one warp per tile, paired rounds on the top tier)
 FULL_CASES = [(K, n, steps, order)
               for K in (0, 1) for n in (3, 4, 8) for steps in (1, 10)
-              for order in ("reference", "lex", "lex-split")]
+              for order in ("reference", "lex", "lex-split")] + \
+             [(1, 5, steps, "reference") for steps in (1, 10)]
 
 
 def _tier_errors(sig, want, tiers):
