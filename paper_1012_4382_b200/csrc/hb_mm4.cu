@@ -95,20 +95,42 @@ __global__ void __launch_bounds__(32, CAP ? 12 : 1) k_mm4(const KParams P) {
 // the reference's; only the grouping of the final sum differs from k_mm4 (equal
 // to the last bits).  The split is chosen from the size of the whole hierarchy,
 // so all shards of a run and the unsharded run use the same one.
-// Measured at the config-3 K = 0 twin (54 tiles): 19.7-20.6 vs 25.5-27.5 us per
-// step; K = 1, N_max = 4 (96 tiles): 26 vs 37; N_max = 5 (364 tiles, 1 + 1): 36
-// vs 43; above ~4 tiles per SM one warp per tile wins (N_max = 6: 58 vs 51).
-template <int D>
-__host__ __device__ constexpr int row_split() {  // balances ~3:1 off-diagonal : diagonal cost
-  int tot = 0;
-  for (int i = 0; i < D; ++i) tot += 3 * (D - 1 - i) + 1;
-  int acc = 0;
-  for (int r = 0; r < D; ++r) {
-    acc += 3 * (D - 1 - r) + 1;
-    if (2 * acc >= tot) return r + 1;
+// Row ranges balance the commutator's cost; sites split at an even index so
+// the paired rounds of top-tier tiles stay pairs.  Measured (us per step, vs
+// k_mm4): config-3 K = 0 twin, 54 tiles, 3 + 2 warps: 17.5 vs 25.5; K = 1,
+// N_max = 4, 96 tiles, 2 + 2: 25.6 vs 37; N_max = 5, 364 tiles, 1 + 1: 36 vs 43;
+// above ~4 tiles per SM one warp per tile wins (N_max = 6, 1,211 tiles: 58 vs
+// 51).  2 + 1 / 1 + 2 / 4 + 1 / 4 + 2 warps were measured too (within 5 %).
+// rows [row_bound(w), row_bound(w + 1)) of the ADO for phase-A warp w of NA:
+// the partition minimising the largest part, row i costing ~3 (d - 1 - i) + 1
+// (off-diagonal elements ~3x a diagonal one)
+template <int D, int NA>
+struct RowSplit {
+  int b[5];
+  __host__ __device__ constexpr RowSplit() : b{0, D, D, D, D} {
+    int best = 1 << 30;
+    auto cost = [](int r0, int r1) {
+      int c = 0;
+      for (int i = r0; i < r1; ++i) c += 3 * (D - 1 - i) + 1;
+      return c;
+    };
+    auto mx = [](int x, int y) { return x > y ? x : y; };
+    for (int x = 0; x <= D; ++x)
+      for (int y = x; y <= D; ++y)
+        for (int z = y; z <= D; ++z) {
+          const int c1 = NA >= 2 ? x : D, c2 = NA >= 3 ? y : D, c3 = NA >= 4 ? z : D;
+          if ((NA < 2 && x) || (NA < 3 && y != x) || (NA < 4 && z != y)) continue;
+          const int m = mx(mx(cost(0, c1), cost(c1, c2)), mx(cost(c2, c3), cost(c3, D)));
+          if (m < best) {
+            best = m;
+            b[1] = c1;
+            b[2] = c2;
+            b[3] = c3;
+          }
+        }
+    b[NA] = D;
   }
-  return D;
-}
+};
 template <int D>
 __host__ __device__ constexpr int site_split() { return ((D + 1) / 2 + 1) / 2 * 2 < D ? ((D + 1) / 2 + 1) / 2 * 2 : D; }
 
@@ -118,7 +140,7 @@ __global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
   constexpr int M = D * KP1;
   constexpr int TB = NP * TILE;
   constexpr bool kInc = kIncScheme<T>;
-  constexpr int RS = NA == 2 ? row_split<D>() : D;
+  constexpr RowSplit<D, NA> RB{};
   constexpr int SS = NB == 2 ? site_split<D>() : D;
   __shared__ __align__(128) T sBase[(STAGE >= 2 || kInc ? NP : 1) * TILE];
   __shared__ __align__(128) T sInc[(kInc && (STAGE == 2 || STAGE == 4) ? NP : 1) * TILE];
@@ -142,10 +164,10 @@ __global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
   __syncthreads();
   pdl_wait();
   if (warp == 0) tile_prologue_late<T, D, STAGE>(P, tile, sInc, &bar);
-  if (ctl->status != ST_RUNNING) {
-    mbar_wait(&bar, 0);
-    return;
-  }
+  // the status after the grid dependency is only tested before the stores, so
+  // the tile's loads do not wait for it (a stopped run's replays compute and
+  // discard; the sink rates written by tile 0 are only read while running)
+  const int status = ctl->status;
   pdl_release();
   const long long step_next = ctl->step + 1;
   T acc[NP];
@@ -175,15 +197,22 @@ __global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
                                                                             sDn, sN, acc);
   };
   using Z = std::integral_constant<int, 0>;
-  using RSc = std::integral_constant<int, RS>;
   using Dc = std::integral_constant<int, D>;
   using SSc = std::integral_constant<int, SS>;
-  if (warp == 0) {
-    phase_a<T, D, KP1, STAGE, 0, RS>(P, tile, lane, c, sBase, sN, &bar, acc);
-    put_rows(Z(), RSc());
-  } else if (NA == 2 && warp == 1) {
-    phase_a<T, D, KP1, STAGE, RS, D>(P, tile, lane, c, sBase, sN, &bar, acc);
-    put_rows(RSc(), Dc());
+  if (warp < NA) {
+    auto part_a = [&](auto w) {
+      constexpr int W = decltype(w)::value;
+      if constexpr (W < NA) {
+        if (warp == W) {
+          phase_a<T, D, KP1, STAGE, RB.b[W], RB.b[W + 1]>(P, tile, lane, c, sBase, sN, &bar, acc);
+          put_rows(std::integral_constant<int, RB.b[W]>(), std::integral_constant<int, RB.b[W + 1]>());
+        }
+      }
+    };
+    part_a(std::integral_constant<int, 0>());
+    part_a(std::integral_constant<int, 1>());
+    part_a(std::integral_constant<int, 2>());
+    part_a(std::integral_constant<int, 3>());
   } else if (NB == 2 && warp == NA) {
     phase_b_part(Z(), SSc());
 #pragma unroll
@@ -193,6 +222,7 @@ __global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
     else phase_b_part(Z(), Dc());
   }
   __syncthreads();
+  if (status != ST_RUNNING) return;  // every warp is past its bulk-copy wait
   if (warp == NA + NB - 1) {
 #pragma unroll
     for (int e = 0; e < NP; ++e)
@@ -278,9 +308,10 @@ static cudaError_t mm4_go(const KParams& p, cudaStream_t s) {
       cfg.blockDim = dim3(64);
       return cudaLaunchKernelEx(&cfg, k_mm4ab<T, D, KP1, STAGE, 1, 1>, p);
     }
-    if (p.split == 2) {
-      cfg.blockDim = dim3(128);
-      return cudaLaunchKernelEx(&cfg, k_mm4ab<T, D, KP1, STAGE, 2, 2>, p);
+    if (p.split == 2) {  // K = 0: 3 + 2 warps; K >= 1 (twice the link crosses): 2 + 2
+      constexpr int NA = KP1 == 1 ? 3 : 2;
+      cfg.blockDim = dim3(32 * (NA + 2));
+      return cudaLaunchKernelEx(&cfg, k_mm4ab<T, D, KP1, STAGE, NA, 2>, p);
     }
   }
   return cudaLaunchKernelEx(&cfg, k_mm4<T, D, KP1, STAGE, CAP>, p);
