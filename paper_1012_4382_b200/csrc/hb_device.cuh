@@ -240,17 +240,11 @@ __device__ __forceinline__ void ctl_store_warp(Ctl* g, const Ctl& cs) {
   __syncwarp();
 }
 
-template <int D, bool HERM>
-__device__ void finish_step_warp(const KParams& P, long long step) {
-  if (!P.root) {
-    finish_step_shard(P, step);
-    return;
-  }
-  __shared__ Sig0 s0;
-  __shared__ Ctl cs;
+// the root bookkeeping on copies already in shared memory (cs: the control
+// block, s0: sigma^0 of the new state); the caller writes cs back
+template <int D>
+__device__ void finish_step_loaded(const KParams& P, long long step, const Sig0& s0, Ctl& cs) {
   const int lane = threadIdx.x & 31;
-  ctl_load_warp(P.ctl, cs);
-  sig0_warp<D, HERM>(P, s0);  // ends with __syncwarp: cs is complete too
   volatile Ctl* c = &cs;
   double m0 = 0.0;
   for (int f = lane; f < D * D; f += 32) m0 = fmax(m0, s0.re[f] * s0.re[f] + s0.im[f] * s0.im[f]);
@@ -277,6 +271,19 @@ __device__ void finish_step_warp(const KParams& P, long long step) {
     if (step % P.stride == 0) record_warp<D>(P, step, s0, c);
     check_stop_warp<D>(P, step, s0, c);
   }
+}
+
+template <int D, bool HERM>
+__device__ void finish_step_warp(const KParams& P, long long step) {
+  if (!P.root) {
+    finish_step_shard(P, step);
+    return;
+  }
+  __shared__ Sig0 s0;
+  __shared__ Ctl cs;
+  ctl_load_warp(P.ctl, cs);
+  sig0_warp<D, HERM>(P, s0);  // ends with __syncwarp: cs is complete too
+  finish_step_loaded<D>(P, step, s0, cs);
   ctl_store_warp(P.ctl, cs);
 }
 

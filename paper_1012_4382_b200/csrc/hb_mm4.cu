@@ -250,17 +250,40 @@ __global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
 // sized for that many).
 template <int D>
 __global__ void __launch_bounds__(32, 1) k_step_finish(const KParams P) {
-  volatile Ctl* ctl = P.ctl;
+  // released only once stage 4 has completed: released earlier, the next
+  // step's stage-1 CTAs would take SM slots from stage 4's last waves
   pdl_wait();
-  if (ctl->status == ST_RUNNING) {
-    pdl_release();
-    const long long step_next = ctl->step + 1;
-    if (threadIdx.x == 0) ctl->launches = ctl->launches + 5;
-    finish_step_warp<D, true>(P, step_next);
+  pdl_release();
+  volatile Ctl* ctl = P.ctl;
+  int status;
+  long long loop_iter;
+  if (!P.root) {  // non-root shard (hb_device.cuh finish_step_shard)
+    if (ctl->status == ST_RUNNING) {
+      const long long step_next = ctl->step + 1;
+      if (threadIdx.x == 0) ctl->launches = ctl->launches + 5;
+      finish_step_warp<D, true>(P, step_next);
+    }
+    __syncwarp();
+    status = ctl->status;
+    loop_iter = ctl->loop_iter;
+  } else {
+    // the control block and sigma^0 in one round trip (both are read even when
+    // the run has stopped: a replay past the stop then writes nothing)
+    __shared__ Sig0 s0;
+    __shared__ Ctl cs;
+    ctl_load_warp(P.ctl, cs);
+    sig0_warp<D, true>(P, s0);
+    if (cs.status == ST_RUNNING) {
+      if (threadIdx.x == 0) cs.launches += 5;
+      finish_step_loaded<D>(P, cs.step + 1, s0, cs);
+      ctl_store_warp(P.ctl, cs);
+    }
+    status = cs.status;
+    loop_iter = cs.loop_iter;
   }
-  if (P.set_cond && threadIdx.x == 0) {  // finish_step_warp ended with __syncwarp
-    const long long it = ctl->loop_iter + 1;
-    const bool again = ctl->status == ST_RUNNING && it < P.loop_iters;
+  if (P.set_cond && threadIdx.x == 0) {
+    const long long it = loop_iter + 1;
+    const bool again = status == ST_RUNNING && it < P.loop_iters;
     ctl->loop_iter = again ? it : 0;
     cudaGraphSetConditional(P.cond, again ? 1u : 0u);
   }
