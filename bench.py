@@ -54,6 +54,8 @@ B_ALG_STEP = 12 * S_PACKED                # algorithmic state bytes per ADO-step
 B_ALG_STAGE = {1: 2 * S_PACKED, 2: 4 * S_PACKED, 3: 3 * S_PACKED, 4: 3 * S_PACKED}
 B_ALG_SINGLE = 15 * 4 * D * D             # precision='single': 15 float passes
 PROFILE = ROOT / "profiles" / "r2_stage_kernels.json"   # ncu --set full of the stage kernels
+L2_STREAM_GBPS = 17242.0         # tools/micro/l2bw.cu: L2-resident 16-B streaming loads, all SMs
+L2_GATHER_SECTOR_GBPS = 9270.0   # random 16-B gathers: one 32-B sector per SM cycle
 REF_DIR = ROOT / "baseline" / "_ref"
 
 
@@ -321,15 +323,16 @@ def ncu_traffic():
     """DRAM bytes per RK4 step of the four stage launches, from the committed
     ncu --set full capture (tools/gpu_profile.sh)."""
     if not PROFILE.exists():
-        return None, "stage kernels", None
+        return None, "stage kernels", None, None
     try:
         launches = json.loads(PROFILE.read_text())["launches"]
         stages = [e for e in launches if "k_mm4" in e["kernel"]]
         traffic = sum(e["dram_total_MB"] for e in stages) * 1e6
         name = " | ".join(e["kernel"].split("(")[0].replace("void ", "") for e in stages)
-        return traffic, name, [round(e["dram_total_MB"], 1) for e in stages]
+        l2 = sum(e.get("l2_MB", 0.0) for e in stages) * 1e6 or None
+        return traffic, name, [round(e["dram_total_MB"], 1) for e in stages], l2
     except (KeyError, ValueError, IndexError):
-        return None, "stage kernels", None
+        return None, "stage kernels", None, None
 
 
 def time_replica(xf, ops, device, args, dist, local, world):
@@ -510,7 +513,7 @@ def run_b200(args):
                 cpu["reference"] = {"error": str(exc)}
 
     if rank == 0:
-        traffic, kname, traffic_stages = ncu_traffic()
+        traffic, kname, traffic_stages, l2_bytes = ncu_traffic()
         achieved = N_ADO * B_ALG_STEP / (ms_step / 1e3) / 1e9
         stage_frac = [round(N_ADO * B_ALG_STAGE[s + 1] / (stage_ms[s] / 1e3) / 1e9 / peak, 3)
                       for s in range(4)]
@@ -532,7 +535,15 @@ def run_b200(args):
                          "stage_frac": stage_frac,
                          "stage_note": "stage_us from events around isolated launches (no PDL "
                                        "overlap), per-stage bytes 2S/4S/3S/3S, S = 392 B",
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+                         # the ceiling the stage kernels actually press on: L2 sector traffic
+                         # (own tile + link gathers + tables + stores), ncu lts__t_sectors
+                         "l2": {"bytes_per_step": l2_bytes,
+                                "achieved_GBps": l2_bytes / (ms_step / 1e3) / 1e9 if l2_bytes else None,
+                                "stream_peak_GBps": L2_STREAM_GBPS,
+                                "random_sector_peak_GBps": L2_GATHER_SECTOR_GBPS,
+                                "source": "ncu lts__t_sectors.sum x 32 B (profiles/r2_stage_kernels.json); "
+                                          "peaks: tools/micro/l2bw.cu on B200 (profiles/r2_l2bw.txt)"}},
             "e2e": {"value": e2e[50]["value"], "unit": UNIT,
                     "h2d_bytes_per_step": int(round(e2e[50]["h2d_bytes_per_step"])),
                     "d2h_bytes_per_step": int(round(e2e[50]["d2h_bytes_per_step"])),

@@ -22,6 +22,8 @@ KEYS = {
     "inst_executed": "smsp__inst_executed.sum",
     "grid": "launch__grid_size",
     "block": "launch__block_size",
+    "l2_sectors": "lts__t_sectors.sum",
+    "l1_global_load_sectors": "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
 }
 UNIT_SCALE = {"Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "byte": 1e-6, "us": 1.0, "ms": 1e3, "ns": 1e-3}
 
@@ -52,6 +54,10 @@ def main():
                 ent["dram_GBps"] = ent["dram_total_MB"] / ent["duration_us"] * 1e3
             if n_ado:
                 ent["dram_bytes_per_ado"] = ent["dram_total_MB"] * 1e6 / n_ado
+        if "l2_sectors" in ent:
+            ent["l2_MB"] = ent["l2_sectors"] * 32 / 1e6
+            if ent.get("duration_us"):
+                ent["l2_GBps"] = ent["l2_MB"] / ent["duration_us"] * 1e3
         launches.append(ent)
     json.dump({"source": raw, "n_ado": n_ado, "launches": launches}, open(out, "w"), indent=1)
     for e in launches:
