@@ -243,7 +243,8 @@ __device__ __forceinline__ void ctl_store_warp(Ctl* g, const Ctl& cs) {
 // the root bookkeeping on copies already in shared memory (cs: the control
 // block, s0: sigma^0 of the new state); the caller writes cs back
 template <int D>
-__device__ void finish_step_loaded(const KParams& P, long long step, const Sig0& s0, Ctl& cs) {
+__device__ void finish_step_loaded(const KParams& P, long long step, const Sig0& s0, Ctl& cs,
+                                   int par) {
   const int lane = threadIdx.x & 31;
   volatile Ctl* c = &cs;
   double m0 = 0.0;
@@ -255,7 +256,8 @@ __device__ void finish_step_loaded(const KParams& P, long long step, const Sig0&
     c->blocks_done = 0;
     c->step = step;
     for (int s = 0; s < P.n_sinks; ++s)
-      c->sink_pops[s] += (P.dt / 6.0) * (c->r[0][s] + 2.0 * (c->r[1][s] + c->r[2][s]) + c->r[3][s]);
+      c->sink_pops[s] += (P.dt / 6.0) * (c->r[par][0][s] + 2.0 * (c->r[par][1][s] + c->r[par][2][s]) +
+                                         c->r[par][3][s]);
     const bool full = step % 25 == 0;
     double mall = 0.0;
     if (full) {
@@ -283,8 +285,34 @@ __device__ void finish_step_warp(const KParams& P, long long step) {
   __shared__ Ctl cs;
   ctl_load_warp(P.ctl, cs);
   sig0_warp<D, HERM>(P, s0);  // ends with __syncwarp: cs is complete too
-  finish_step_loaded<D>(P, step, s0, cs);
+  finish_step_loaded<D>(P, step, s0, cs, P.rpar);
   ctl_store_warp(P.ctl, cs);
+}
+
+// The bookkeeping of the previous step done by the extra CTA of a stage-1 launch
+// (KParams::fold), while the tiles compute that stage: it reads the
+// control block and sigma^0 as k_step_finish does, takes the sink rates of the
+// previous step's parity, and writes back only the fields the bookkeeping owns
+// (tile 0 of this launch writes this step's sink rates concurrently).
+template <int D>
+__device__ void fold_finish_warp(const KParams& P) {
+  __shared__ Sig0 s0;
+  __shared__ Ctl cs;
+  ctl_load_warp(P.ctl, cs);
+  sig0_warp<D, true>(P, s0);
+  if (cs.status != ST_RUNNING) return;
+  if ((threadIdx.x & 31) == 0) cs.launches += 4;  // this step's four stage kernels
+  finish_step_loaded<D>(P, cs.step + 1, s0, cs, P.rpar ^ 1);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    Ctl* g = P.ctl;
+    for (int s = 0; s < MAXS; ++s) __stcg(&g->sink_pops[s], cs.sink_pops[s]);
+    __stcg(&g->maxabs2_bits, cs.maxabs2_bits);
+    __stcg(&g->n_rec, cs.n_rec);
+    __stcg(&g->launches, cs.launches);
+    __stcg(&g->step, cs.step);
+    __stcg(&g->status, cs.status);
+  }
 }
 
 // t = 0 sample + stop policy before the first step (heom.py:355-368); 1 warp

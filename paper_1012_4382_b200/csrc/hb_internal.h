@@ -52,7 +52,8 @@ struct Ctl {
   int pad0;
   long long step;
   double sink_pops[MAXS];
-  double r[4][MAXS];                  // sink rates of the four stage inputs
+  double r[2][4][MAXS];               // sink rates of the four stage inputs, by step parity
+                                      // (KParams::rpar; the folded bookkeeping reads the last step's)
   unsigned long long maxabs2_bits;    // max |x|^2 over all ADOs (every 25 steps)
   unsigned int blocks_done;           // last-block election counter
   unsigned int pad1;
@@ -85,6 +86,10 @@ struct KParams {
   const uint8_t* nvec;
   const double* damp_plane;  // optional per-ADO damping (Level-2 shim), else null
   int fast;                  // production kernel k_mm4 (hb_mm4.cu), else the generic k_stage
+  int rpar;                  // step parity of this launch: which ctl->r the stage writes
+  int fold;                  // k_mm4ab graphs: stage 1 also does the previous step's
+                             // bookkeeping (an extra warp of CTA 0); stage 4 then has no
+                             // k_step_finish after it
   int split;                 // small hierarchies (fast path, d <= 7): a tile's phase A and
                              // phase B on separate warps, k_mm4ab: 1 = 1 + 1 warps,
                              // 2 = 2 + 2 warps; 0 = k_mm4 (one warp per tile)

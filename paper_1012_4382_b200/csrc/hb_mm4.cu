@@ -134,7 +134,7 @@ struct RowSplit {
 template <int D>
 __host__ __device__ constexpr int site_split() { return ((D + 1) / 2 + 1) / 2 * 2 < D ? ((D + 1) / 2 + 1) / 2 * 2 : D; }
 
-template <class T, int D, int KP1, int STAGE, int NA, int NB>
+template <class T, int D, int KP1, int STAGE, int NA, int NB, bool FOLD = false>
 __global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
   constexpr int NP = D * D;
   constexpr int M = D * KP1;
@@ -153,6 +153,18 @@ __global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
   volatile Ctl* ctl = P.ctl;
   if (ctl->status != ST_RUNNING) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // a separate instantiation: the bookkeeping code (~20 KB of SASS) in every
+  // stage-1 kernel costs ~5 % through the instruction cache when unused
+  if constexpr (FOLD) {
+  if (blockIdx.x == gridDim.x - 1) {
+    // the extra CTA of a folded stage 1: the previous step's bookkeeping, on an
+    // SM of its own, while the tiles compute
+    pdl_wait();
+    pdl_release();
+    if (warp == 0) fold_finish_warp<D>(P);
+    return;
+  }
+  }
   const int tile = P.tile_list ? P.tile_list[blockIdx.x] : P.tile_begin + blockIdx.x;
   HB_CHECK(tile >= 0 && tile < P.n_tiles_total);
   const size_t tb = (size_t)tile * TB;
@@ -275,7 +287,7 @@ __global__ void __launch_bounds__(32, 1) k_step_finish(const KParams P) {
     sig0_warp<D, true>(P, s0);
     if (cs.status == ST_RUNNING) {
       if (threadIdx.x == 0) cs.launches += 5;
-      finish_step_loaded<D>(P, cs.step + 1, s0, cs);
+      finish_step_loaded<D>(P, cs.step + 1, s0, cs, P.rpar);
       ctl_store_warp(P.ctl, cs);
     }
     status = cs.status;
@@ -327,14 +339,19 @@ static cudaError_t mm4_go(const KParams& p, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = n;
   if constexpr (D <= 7) {  // (41.5 KB of static shared memory at d = 7, 2 + 2 warps)
+    constexpr bool kFold = STAGE == 1 && KP1 == 1;  // (hb_api.cu folds only at K = 0)
+    const bool fold = kFold && p.fold;
+    if (fold) cfg.gridDim.x += 1;  // the folded bookkeeping CTA
     if (p.split == 1) {
       cfg.blockDim = dim3(64);
-      return cudaLaunchKernelEx(&cfg, k_mm4ab<T, D, KP1, STAGE, 1, 1>, p);
+      return cudaLaunchKernelEx(&cfg, fold ? k_mm4ab<T, D, KP1, STAGE, 1, 1, kFold>
+                                           : k_mm4ab<T, D, KP1, STAGE, 1, 1>, p);
     }
     if (p.split == 2) {  // K = 0: 3 + 2 warps; K >= 1 (twice the link crosses): 2 + 2
       constexpr int NA = KP1 == 1 ? 3 : 2;
       cfg.blockDim = dim3(32 * (NA + 2));
-      return cudaLaunchKernelEx(&cfg, k_mm4ab<T, D, KP1, STAGE, NA, 2>, p);
+      return cudaLaunchKernelEx(&cfg, fold ? k_mm4ab<T, D, KP1, STAGE, NA, 2, kFold>
+                                           : k_mm4ab<T, D, KP1, STAGE, NA, 2>, p);
     }
   }
   return cudaLaunchKernelEx(&cfg, k_mm4<T, D, KP1, STAGE, CAP>, p);
@@ -360,7 +377,7 @@ template <int D, int KP1>
 static cudaError_t mm4_t(int stage, const KParams& p, cudaStream_t s) {
   const cudaError_t e = p.single ? mm4_stage<float, D, KP1>(stage, p, s)
                                  : mm4_stage<double, D, KP1>(stage, p, s);
-  if (e != cudaSuccess || stage != 4) return e;
+  if (e != cudaSuccess || stage != 4 || p.fold) return e;  // folded: the next stage 1 finishes
   return finish_go<D>(p, s);
 }
 

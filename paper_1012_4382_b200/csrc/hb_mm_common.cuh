@@ -156,7 +156,7 @@ __device__ __forceinline__ void phase_a(const KParams& P, int tile, int lane, T 
         const double v = P.sink_rate[q] * (double)__ldg(st_in<T>(P) + P.sink_pos[q] * TILE);
         a = cc == 0 ? v : a + v;
       }
-      ctl->r[STAGE - 1][sk] = a;
+      ctl->r[P.rpar][STAGE - 1][sk] = a;
     }
   }
   mbar_wait(bar, 0);

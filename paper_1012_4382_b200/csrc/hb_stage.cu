@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(D * 32) k_stage(const KParams P) {
         const double v = P.sink_rate[t] * s_re[p][p][0];
         acc = cc == 0 ? v : acc + v;
       }
-      ctl->r[STAGE - 1][s] = acc;
+      ctl->r[P.rpar][STAGE - 1][s] = acc;
     }
   }
 
