@@ -998,12 +998,12 @@ int hb_set_state(hb_handle* h, const double* sig, const double* sink_pops) {
 static cudaError_t capture_steps(hb_handle* h, int n_steps, bool set_cond,
                                  cudaGraphConditionalHandle cond) {
   cudaError_t err = cudaSuccess;
-  // k_mm4ab graphs at K = 0 fold each step's bookkeeping into the next step's
-  // stage 1 (an extra CTA; one launch less per step), except the last step of
-  // the graph, whose k_step_finish closes the body; the sink rates alternate by
-  // step parity.  (K = 0 twin: 17.5 -> 15.4 us per step; at K = 1 it measured
-  // 3-5 % slower, N_max = 4 and 5, so K >= 1 keeps the separate kernel.)
-  const bool fold = h->base.fast && h->base.split && h->base.kp1 == 1;
+  // k_mm4ab graphs fold each step's bookkeeping into the next step's stage 1
+  // (an extra CTA; one launch less per step), except the last step of the
+  // graph, whose k_step_finish closes the body; the sink rates alternate by
+  // step parity.  (us per step: K = 0 twin 17.5 -> 15.4; K = 1, N_max = 4
+  // 24.0 -> 21.4; N_max = 5 34.4 -> 32.0.)
+  const bool fold = h->base.fast && h->base.split;
   for (int c = 0; c < n_steps && !err; ++c)
     for (int s = 1; s <= 4 && !err; ++s) {
       KParams p = stage_params(h, s);

@@ -151,7 +151,14 @@ __global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
   __shared__ __align__(16) uint8_t sN[M][TILE];
   __shared__ __align__(8) uint64_t bar;
   volatile Ctl* ctl = P.ctl;
-  if (ctl->status != ST_RUNNING) return;
+  // the early exit must be one decision per CTA: the status can change while
+  // the CTA starts (the previous step's bookkeeping runs concurrently under PDL,
+  // or in this very launch when folded), and a warp that went on alone would
+  // wait on a barrier nobody initialised
+  __shared__ int s_stopped;
+  if (threadIdx.x == 0) s_stopped = ctl->status != ST_RUNNING;
+  __syncthreads();
+  if (s_stopped) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // a separate instantiation: the bookkeeping code (~20 KB of SASS) in every
   // stage-1 kernel costs ~5 % through the instruction cache when unused
@@ -339,7 +346,7 @@ static cudaError_t mm4_go(const KParams& p, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = n;
   if constexpr (D <= 7) {  // (41.5 KB of static shared memory at d = 7, 2 + 2 warps)
-    constexpr bool kFold = STAGE == 1 && KP1 == 1;  // (hb_api.cu folds only at K = 0)
+    constexpr bool kFold = STAGE == 1;
     const bool fold = kFold && p.fold;
     if (fold) cfg.gridDim.x += 1;  // the folded bookkeeping CTA
     if (p.split == 1) {
