@@ -163,14 +163,14 @@ __global__ void __launch_bounds__(32 * (NA + NB), 1) k_mm4ab(const KParams P) {
   // a separate instantiation: the bookkeeping code (~20 KB of SASS) in every
   // stage-1 kernel costs ~5 % through the instruction cache when unused
   if constexpr (FOLD) {
-  if (blockIdx.x == gridDim.x - 1) {
-    // the extra CTA of a folded stage 1: the previous step's bookkeeping, on an
-    // SM of its own, while the tiles compute
-    pdl_wait();
-    pdl_release();
-    if (warp == 0) fold_finish_warp<D>(P);
-    return;
-  }
+    if (blockIdx.x == gridDim.x - 1) {
+      // the extra CTA of a folded stage 1: the previous step's bookkeeping, on
+      // an SM of its own, while the tiles compute
+      pdl_wait();
+      pdl_release();
+      if (warp == 0) fold_finish_warp<D>(P);
+      return;
+    }
   }
   const int tile = P.tile_list ? P.tile_list[blockIdx.x] : P.tile_begin + blockIdx.x;
   HB_CHECK(tile >= 0 && tile < P.n_tiles_total);
