@@ -19,6 +19,10 @@
 //     4 dependent L2 round trips instead of 7.
 // T = double (HB_PREC_DOUBLE) or float (HB_PREC_SINGLE: float state, float RHS,
 // heom.py:93-94; bookkeeping, sinks and records stay double).
+//
+// Small hierarchies (KParams::split) use k_mm4ab below instead: the same phases
+// on separate warps of one CTA per tile, and in CUDA graphs the previous step's
+// bookkeeping folded into stage 1 as an extra CTA (KParams::fold).
 #include "hb_device.cuh"
 #include "hb_mm_common.cuh"
 
