@@ -59,10 +59,10 @@ __global__ void __launch_bounds__(32, CAP ? 12 : 1) k_mm4(const KParams P) {
                                   sInc, true);
   pdl_wait();
   tile_prologue_late<T, D, STAGE>(P, tile, sInc, &bar);
-  if (ctl->status != ST_RUNNING) {
-    mbar_wait(&bar, 0);  // no bulk copy may land after the CTA has exited
-    return;
-  }
+  // the status after the grid dependency is tested before the stores only, so
+  // the loads below do not wait for it (replays after the stop already exited
+  // at the first test; this one catches a stop landing while the CTA started)
+  const int status = ctl->status;
   pdl_release();
   const long long step_next = ctl->step + 1;
   T acc[NP];
@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(32, CAP ? 12 : 1) k_mm4(const KParams P) {
     no_up = !__any_sync(0xffffffffu, up_any);
   }
   phase_b_sites<T, D, KP1>(P, lane, c, no_up, sUp, sDn, sN, acc);
+  if (status != ST_RUNNING) return;  // past the bulk-copy wait (phase A)
   double maxa2 = 0.0;
   phase_c_store<T, D, STAGE>(P, lane, tb, sBase, acc, maxa2, sInc);
   if (STAGE == 4 && step_next % 25 == 0) {  // whole-state guard (heom.py:386-389)

@@ -1,6 +1,4 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-for r in 1 2; do for v in v0 s2x2; do
-  HB_PROBE_NMAX=8 HEOM_B200_LIB=$PWD/exp_build/$v/libheomb200.so python tools/small_probe.py 0 2000 2>&1 | grep "end to end" | sed "s/^/[$v] /"
-  HB_PROBE_NMAX=7 HEOM_B200_LIB=$PWD/exp_build/$v/libheomb200.so python tools/small_probe.py 0 2000 2>&1 | grep "end to end" | sed "s/^/[$v] /"
-done; done
+timeout 2400 python -m pytest tests -m gpu -q -x -p no:cacheprovider > /tmp/t.log 2>&1; tail -1 /tmp/t.log; grep -A40 "^____" /tmp/t.log | head -50
+HEOM_B200_LIB=$PWD/paper_1012_4382_b200/libheomb200_checked.so timeout 2400 python -m pytest tests -m gpu -q -x -p no:cacheprovider > /tmp/t.log 2>&1; tail -1 /tmp/t.log; grep -A40 "^____" /tmp/t.log | head -50
